@@ -1,0 +1,344 @@
+#!/usr/bin/env python3
+"""bench.py -- massive-PRNG hot path (arXiv 1609.01257 §5) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] ...
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+One "step" = one pass of the whole hot path over one synthetic workload:
+prng_init (a1, seeding kernel) + prng_generate(numiter) (a2+a3: xorshift64 batch kernel,
+register-resident state, 32-byte stores into a device ring).  BASELINE.json's metric is
+random numbers/s (and GB/s, 8 B per number, Eq. 1) device-only and end to end.
+
+* value      device-only numbers/s over all ranks: inputs (numrn, numiter, seed) resident,
+             output ring (>= 2 GiB, > 16x the 126 MB L2, so no L2 flush is needed) in HBM.
+             Timed with CUDA events on the generation stream (a torch stream handed to the
+             library), K steps between barrier + synchronize, max over ranks.
+* e2e        same metric through the C-ABI call with HOST buffers: prng_generate with the
+             null sink (the paper discards stdout), i.e. device ring -> D2H on a side
+             stream -> pinned host double buffer -> sink, all inside the timed region.
+* roofline   dominant kernel (the batch kernel): algorithmic bytes per launch
+             (8 B x numbers) / mean launch duration from CUDA events on its stream,
+             against MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline  the oracle (oracle/, plain single-threaded C) on a bounded sample.
+
+Rank r of N owns the contiguous gid range shard_range(numrn_total, r, N) (weak scaling:
+numrn per GPU fixed, default 2^24).  The only collectives are a barrier and a MAX
+all-reduce of the elapsed times.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import SEED_PERF, shard_range  # noqa: E402
+
+DEF_NUMRN = 1 << 24
+DEF_NUMITER = 1000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--numrn-per-gpu", type=int, default=DEF_NUMRN)
+    ap.add_argument("--numrn-total", type=int, default=0, help="strong scaling: fixed total numrn (e.g. 2^28)")
+    ap.add_argument("--numiter", type=int, default=DEF_NUMITER)
+    ap.add_argument("--seed", type=int, default=SEED_PERF)
+    ap.add_argument("--kernel", type=int, default=0, help="kernel variant id")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-warmup", type=int, default=1)
+    ap.add_argument("--e2e-mode", type=int, default=3, help="0 S0, 1 S1, 2 O1, 3 O2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-probes", action="store_true")
+    ap.add_argument("--cpu-numiter", type=int, default=64, help="oracle sample: numiter at full numrn")
+    ap.add_argument("--ref-numiter", type=int, default=8, help="--impl reference: numiter per step sample")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- distributed plumbing
+class Dist:
+    def __init__(self, backend):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = None
+        if self.world > 1 and backend:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.dist:
+            return x
+        import torch
+        dev = "cuda" if self.dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- clocks during timing
+class Clocks:
+    """nvidia-smi sampled every 100 ms while the timed region runs (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: copy, read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the batch kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_batch_kernel.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+
+
+# ---------------------------------------------------------------- oracle timing (CPU)
+def cpu_baseline(numrn, numiter, seed):
+    import oracle
+    t = time.perf_counter()
+    oracle.digest(numrn, numiter, seed)
+    dt = time.perf_counter() - t
+    return numrn * numiter / dt, dt
+
+
+def run_reference(a, D):
+    """--impl reference: the oracle as it stands, on the host cores, rank 0 only."""
+    if D.rank != 0:
+        return
+    import oracle
+    oracle.build()
+    numrn = a.numrn_total or a.numrn_per_gpu * D.world
+    ni = a.ref_numiter
+    for _ in range(a.warmup):
+        oracle.digest(numrn, ni, a.seed)
+    t = time.perf_counter()
+    for _ in range(a.steps):
+        oracle.digest(numrn, ni, a.seed)
+    dt = time.perf_counter() - t
+    v = numrn * ni * a.steps / dt
+    sample = f"numrn={numrn} x numiter={ni} per step (of the workload's numiter={a.numiter}); digest-folded"
+    print(json.dumps({
+        "impl": "reference", "metric": "random numbers/s (device-only, 8 B/number)", "value": v,
+        "unit": "numbers/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"numrn={numrn}, numiter={a.numiter}, seed={a.seed} (sampled)"},
+        "cpu_baseline": {"value": v, "unit": "numbers/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "numbers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(a, D):
+    import torch
+    import paper_1609_01257_b200 as P
+
+    torch.cuda.set_device(D.local)
+    numrn = a.numrn_total or a.numrn_per_gpu * D.world
+    gb, cnt = shard_range(numrn, D.rank, D.world)
+    gen = torch.cuda.Stream()
+    cop = torch.cuda.Stream()
+    h = P.prng_create_range(numrn, a.seed, gb, cnt, D.local)
+    P.prng_set_streams(h, gen.cuda_stream, cop.cuda_stream)
+    P.prng_set_option(h, P.PRNG_OPT_KERNEL, a.kernel)
+    P.prng_set_option(h, P.PRNG_OPT_MODE, a.e2e_mode)
+
+    # ---- device only
+    for _ in range(a.warmup):
+        P.prng_init(h)
+        P.prng_generate(h, a.numiter)
+    P.prng_set_option(h, P.PRNG_OPT_PROFILE, 1)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kern_ms, init_ms, launches = [], [], 0
+    with Clocks(D.local) as clk:
+        D.barrier()
+        torch.cuda.synchronize()
+        ev0.record(gen)
+        for _ in range(a.steps):
+            P.prng_init(h)
+            P.prng_generate(h, a.numiter)
+            ids, s, e, _ = P.prng_prof_events(h)  # per-launch CUDA-event intervals of this step
+            kern_ms += [1e3 * (y - x) for i, x, y in zip(ids, s, e) if i == 1]
+            init_ms += [1e3 * (y - x) for i, x, y in zip(ids, s, e) if i == 0]
+            launches += len(ids)
+        ev1.record(gen)
+        torch.cuda.synchronize()
+        D.barrier()
+    ms = ev0.elapsed_time(ev1)
+    P.prng_set_option(h, P.PRNG_OPT_PROFILE, 0)
+    ms_max = D.max(ms)
+    numbers = numrn * a.numiter * a.steps
+    value = numbers / (ms_max * 1e-3)
+    clocks = clk.summary()
+
+    peak, peak_src = measured_peaks()
+    kmean = statistics.mean(kern_ms)
+    algo_bytes = 8 * cnt * a.numiter
+    achieved = algo_bytes / (kmean * 1e-3) / 1e9
+    traffic, _ = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "prngk::batch_kernel<" + P.prng_kernel_variant_name(a.kernel) + ">",
+                "algorithmic_bytes_per_launch": algo_bytes, "mean_launch_ms": kmean,
+                "kernel_share_of_step": sum(kern_ms) / ms, "init_kernel_mean_ms": statistics.mean(init_ms),
+                "peak_source": peak_src}
+
+    # ---- end to end (host buffers, D2H inside the timed region)
+    e2e = None
+    if not a.no_e2e:
+        for _ in range(a.e2e_warmup):
+            P.prng_init(h)
+            P.prng_generate(h, a.numiter, P.SINK_NULL)
+        P.prng_set_option(h, P.PRNG_OPT_PROFILE, 1)
+        walls, prof = [], None
+        for _ in range(a.e2e_steps):
+            D.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            P.prng_init(h)
+            P.prng_generate(h, a.numiter, P.SINK_NULL)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+            prof = P.prng_prof_events(h)
+        P.prng_set_option(h, P.PRNG_OPT_PROFILE, 0)
+        wall = D.max(sum(walls))
+        ev = numrn * a.numiter * a.e2e_steps / wall
+        ids, s, e, w = prof
+        calc = P.prng_prof_calc(ids, s, e, 4)
+        agg = calc["agg"]
+        ov = calc["overlap"]
+        d2h_gbs = 8 * cnt * a.numiter * a.e2e_steps / sum(walls) / 1e9
+        e2e = {"value": ev, "unit": "numbers/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": 8 * numrn * a.numiter, "gbs": 8 * ev / 1e9,
+               "mode": ["S0", "S1", "O1", "O2"][a.e2e_mode], "d2h_gbs_per_gpu": d2h_gbs,
+               "profile_last_step": {
+                   "rng_kernel_s": agg[1], "read_buffer_s": agg[2], "out_s": agg[3], "init_s": agg[0],
+                   "rng_read_overlap_s": ov[1, 2],
+                   "rng_hidden_frac": (ov[1, 2] / agg[1]) if agg[1] else None,
+                   "copy_busy_frac": agg[2] / w if w else None, "effective_s": calc["effective"], "wall_s": w}}
+    probes = None
+    if not a.no_probes and D.rank == 0:
+        probes = {"memset_write_gbs": P.prng_probe_memset_gbs(4 << 30, 5),
+                  "store_kernel_write_gbs": P.prng_probe_store_gbs(4 << 30, 5),
+                  "d2h_pinned_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 1),
+                  "d2h_pinned_2streams_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 2)}
+        if e2e:
+            e2e["roofline"] = {"bound": "host-link", "achieved": e2e["d2h_gbs_per_gpu"],
+                               "peak": probes["d2h_pinned_gbs"], "unit": "GB/s",
+                               "frac": e2e["d2h_gbs_per_gpu"] / probes["d2h_pinned_gbs"],
+                               "peak_source": "same-box pinned cudaMemcpyAsync D2H 1 GiB, best of 5"}
+    P.prng_destroy(h)
+
+    cpu = None
+    if D.rank == 0 and D.world == 1 and not a.no_cpu:
+        v, dt = cpu_baseline(numrn, a.cpu_numiter, a.seed)
+        cpu = {"value": v, "unit": "numbers/s", "cores": 1, "kind": "oracle",
+               "sample": f"numrn={numrn} x numiter={a.cpu_numiter} ({dt:.1f} s, digest-folded, 1 thread)"}
+
+    if D.rank == 0:
+        line = {
+            "metric": "random numbers/s (device-only, 8 B/number)", "value": value, "unit": "numbers/s",
+            "gbs": 8 * value / 1e9, "n_gpus": D.world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+            "scaling": "strong" if a.numrn_total else "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (numrn, numiter, seed); outputs are the generated u64 stream",
+            "config": {"workload": (f"BASELINE config 2: numrn=2^{numrn.bit_length() - 1} ({numrn}) per iteration"
+                                    f" x numiter={a.numiter}, device-only" if D.world == 1 else
+                                    f"numrn={numrn} total ({cnt} per GPU, gid-range sharded) x numiter={a.numiter}"),
+                       "numrn": numrn, "numiter": a.numiter, "seed": a.seed, "parallelism": f"gid-shard{D.world}",
+                       "l2": "output ring >= 2 GiB per GPU (> 16x L2), written once per iteration; no flush needed"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, "probes": probes,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    D = Dist(None if a.impl == "reference" else "nccl")
+    try:
+        if a.impl == "reference":
+            run_reference(a, D)
+        else:
+            run_ours(a, D)
+    finally:
+        D.close()
+
+
+if __name__ == "__main__":
+    main()

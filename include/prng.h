@@ -1,0 +1,192 @@
+/*
+ * prng.h -- C ABI of the B200-native massive-PRNG hot path.
+ *
+ * What it computes (the paper's §5 example application, arXiv 1609.01257):
+ *   "each work-item generates a 64-bit random value per invocation. The init kernel
+ *    creates the initial random values by applying a hash function [wang1997inthash]
+ *    to the global ID of the associated work-items. The generated values not only
+ *    constitute the first batch of random numbers, but also serve as seeds for the
+ *    next batch."                                                   (§5)
+ *   "... a simple Xorshift PRNG [marsaglia2003xorshift]"           (§5)
+ *   n numbers per iteration, i iterations, N = 8*n*i bytes          (Eq. 1)
+ * The exact arithmetic (readings A1-A8 of DESIGN.md §3) is:
+ *   out[0][g] = seed64(g, seed)           (Wang hash of the global id, 0 -> 1)
+ *   out[k][g] = xorshift64(out[k-1][g])   (x^=x<<13; x^=x>>7; x^=x<<17), k = 1..numiter-1
+ * Output layout: iteration-major, gid ascending, little-endian u64 (A8): exactly the
+ * paper's binary stdout stream.
+ *
+ * Conventions follow cf4ocl's (§4.1): an opaque object with a create/destroy
+ * pair; functions take the object first; every fallible call returns a status (0 ok,
+ * < 0 error) AND fills an optional detail object passed last (may be NULL); an errors
+ * module maps codes to strings.
+ *
+ * Ownership: the handle owns all device memory (state array, device ring), pinned host
+ * buffers, CUDA streams and events it creates.  Pointers passed to a sink are BORROWED:
+ * valid only for the duration of the callback ("automatically released and should not
+ * be destroyed by client code").
+ *
+ * Thread-safety: one handle must not be used from two threads at once.  Distinct
+ * handles (e.g. one per GPU / rank) are independent.
+ *
+ * There is no CPU fallback: every generation step runs in the sm_100a kernels of
+ * libprng_b200.so; without a CUDA device prng_create fails with PRNG_ECUDA.
+ */
+#ifndef PRNG_B200_H
+#define PRNG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ errors */
+#define PRNG_OK 0
+#define PRNG_EINVAL -1  /* bad argument (numrn = 0 or > 2^32, numiter = 0, bad range/option) */
+#define PRNG_ESTATE -2  /* bad state: generate before init, or handle poisoned by an abort   */
+#define PRNG_ENOMEM -3  /* device or pinned host allocation failed                          */
+#define PRNG_ECUDA -4   /* CUDA runtime error; detail holds cudaGetErrorString()           */
+#define PRNG_ESINK -5   /* the sink returned nonzero: generation aborted                    */
+
+/* Optional detail object, last argument of every fallible call. */
+typedef struct prng_err {
+    int code;
+    char msg[256];
+} prng_err_t;
+
+/* Total function: unknown codes map to "unknown error <code>". */
+const char *prng_strerror(int code);
+
+/* ------------------------------------------------------------------ handle */
+typedef struct prng prng_t;
+
+/* Sink ("out"): receives `iters` consecutive iterations starting at
+ * iteration `iter_begin`, each `count` u64 for gids [gid_begin, gid_begin + count),
+ * as data[t * count + j] (dense, iteration-major).  `data` is borrowed (pinned host
+ * memory owned by the library).  Called on the caller's thread, strictly in iteration
+ * order.  Return 0 to continue; nonzero aborts prng_generate with PRNG_ESINK. */
+typedef int (*prng_sink_fn)(void *user, uint64_t iter_begin, uint32_t iters,
+                            uint64_t gid_begin, uint64_t count, const uint64_t *data);
+
+/* One generator over all numrn work-items, on the current CUDA device.
+ * numrn in [1, 2^32] (the paper's numrn is a cl_uint).  seed: 0 reproduces the
+ * paper (which has no seed); other values premix into the hash keys (A4).
+ * Returns NULL on error (err filled). */
+prng_t *prng_create(uint64_t numrn, uint64_t seed, prng_err_t *err);
+
+/* A rank's share: the gids [gid_begin, gid_begin + gid_count) of a numrn_total stream,
+ * on CUDA device `cuda_device` (-1 = current).  Values depend only on the GLOBAL gid,
+ * so shards reassemble bit-exactly into the single-device stream (A11). */
+prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begin,
+                          uint64_t gid_count, int cuda_device, prng_err_t *err);
+
+/* NULL-safe.  Synchronises the handle's streams, frees device + pinned memory. */
+void prng_destroy(prng_t *h);
+
+/* Use caller-owned CUDA streams (cudaStream_t, e.g. torch.cuda.Stream().cuda_stream) for
+ * generation and D2H instead of the handle's own; the caller keeps ownership and must
+ * keep them alive until prng_destroy.  The two must differ. */
+int prng_set_streams(prng_t *h, void *gen_stream, void *copy_stream, prng_err_t *err);
+
+/* a1 -- the init kernel: state[g] = seed64(g, seed) on the device; the stream
+ * position is reset to iteration 0 (the next iteration emitted is the seeds themselves). */
+int prng_init(prng_t *h, prng_err_t *err);
+
+/* a2-a5 -- emit the next `numiter` iterations (numiter >= 1).
+ *  sink != NULL (end to end): batches of T iterations are generated into a device ring,
+ *    copied D2H on a side stream into a pinned host double buffer and handed to `sink`
+ *    while the next batches are generated and copied (P:164-173, P:177 limitation 2).
+ *  sink == NULL (device only): iterations are generated into the handle's device ring of
+ *    R slots (slot = iteration mod R) with no host transfer; see prng_device_ring().
+ * Repeated calls continue the stream: generate(a); generate(b) == generate(a + b) (A10).
+ * Blocks until all work of the call is complete. */
+int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, prng_err_t *err);
+
+/* Device-only generation into a caller-owned device buffer (e.g. a torch tensor):
+ * iteration t of this call goes to dst + (t mod dst_slots) * dst_pitch (u64 elements).
+ * dst must be 32-byte aligned and dst_pitch a multiple of 4 with dst_pitch >= count.
+ * Enqueued on `stream` (a cudaStream_t, NULL = the handle's generation stream);
+ * asynchronous: returns after enqueueing. */
+int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch,
+                         uint64_t dst_slots, void *stream, prng_err_t *err);
+
+/* The handle's device ring (device-only mode): base pointer, pitch (u64 elements), number
+ * of slots, and the iteration held by slot 0 .. slots-1 is `iteration mod slots`.
+ * `last_iter_end` = stream position (iterations emitted so far). */
+int prng_device_ring(const prng_t *h, uint64_t **base, uint64_t *pitch, uint64_t *slots,
+                     uint64_t *last_iter_end, prng_err_t *err);
+
+/* Copy `count` outputs of device-ring slot `slot` to host memory (test/inspection aid). */
+int prng_read_slot(prng_t *h, uint64_t slot, uint64_t *host_dst, prng_err_t *err);
+
+/* Copy the current per-gid state (== the last emitted iteration) to host memory. */
+int prng_read_state(prng_t *h, uint64_t *host_dst, prng_err_t *err);
+
+/* ------------------------------------------------------------------ options */
+enum prng_option {
+    PRNG_OPT_MODE = 1,         /* enum prng_mode, default PRNG_MODE_OVERLAP2            */
+    PRNG_OPT_BATCH_ITERS = 2,  /* T for end-to-end batches; 0 = auto (~256 MiB per batch) */
+    PRNG_OPT_RING_SLOTS = 3,   /* R of the device-only ring; 0 = auto (>= 16x L2 bytes)   */
+    PRNG_OPT_PROFILE = 4,      /* 1 = record per-batch intervals (CUDA events)           */
+    PRNG_OPT_KERNEL = 5,       /* kernel variant id (see prng_kernel_variants); 0 = default */
+    PRNG_OPT_GRID_WARPS = 6    /* cap on resident warps of the persistent grid; 0 = auto  */
+};
+
+/* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two
+ * overlapped fixes. */
+enum prng_mode {
+    PRNG_MODE_SERIAL = 0,    /* S0: generate, copy and sink back to back on one stream          */
+    PRNG_MODE_PAGEABLE = 1,  /* S1: side stream, but pageable (malloc) host buffers             */
+    PRNG_MODE_OVERLAP1 = 2,  /* O1: side copy stream + device double buffer, ONE pinned host
+                                buffer: read and out serialised as in the paper */
+    PRNG_MODE_OVERLAP2 = 3   /* O2: O1 + host-side dual buffer, sink(j) || D2H(j+1) || gen(j+2) */
+};
+
+int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err);
+int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err);
+
+/* Number of kernel variants compiled in, and the name of one ("v4n8" = 32-byte stores,
+ * 8 numbers per thread). */
+int prng_kernel_variants(void);
+const char *prng_kernel_variant_name(int id);
+
+/* ------------------------------------------------------------------ profiling (a6) */
+/* Event name ids, as cf4ocl names them in Fig. 3 plus the host sink. */
+#define PRNG_EV_INIT_KERNEL 0
+#define PRNG_EV_RNG_KERNEL 1
+#define PRNG_EV_READ_BUFFER 2
+#define PRNG_EV_OUT 3
+#define PRNG_EV_NAMES 4
+const char *prng_event_name(uint32_t id);
+
+/* Intervals recorded by the last prng_init + prng_generate with PRNG_OPT_PROFILE on:
+ * name id, start and end in seconds from a common origin (device intervals from CUDA
+ * events; OUT intervals from the host clock aligned to the same origin).  `n_out` gets
+ * the number available; at most `cap` are written.  `wall_s` (may be NULL) gets the host
+ * wall time of the profiled calls. */
+int prng_prof_events(const prng_t *h, uint64_t cap, uint32_t *name_id, double *start_s,
+                     double *end_s, uint64_t *n_out, double *wall_s, prng_err_t *err);
+
+/* cf4ocl's ccl_prof_calc arithmetic over arbitrary intervals:
+ *  agg_abs[nnames]          sum of durations per name                       (CCLProfAgg)
+ *  overlap[nnames*nnames]   overlap[a*nnames+b] (a <= b): total pairwise intersection
+ *                           of distinct events named a and b                 (CCLProfOverlap)
+ *  effective                measure of the union of all intervals ("eff.", Fig. 3)
+ *  elapsed_out              = elapsed if elapsed > 0 else max end - min start
+ * Plain host arithmetic (endpoint sweep, O(E log E + S * nnames^2)); no GPU needed. */
+int prng_prof_calc(uint64_t nevents, const uint32_t *name_id, const double *start_s,
+                   const double *end_s, uint32_t nnames, double elapsed, double *agg_abs,
+                   double *overlap, double *effective, double *elapsed_out, prng_err_t *err);
+
+/* ------------------------------------------------------------------ roofline probes */
+/* Same-box denominators: each returns GB/s (best of `reps`) or < 0 on
+ * error.  bytes: buffer size. */
+double prng_probe_memset_gbs(uint64_t bytes, int reps);        /* cudaMemsetAsync write BW  */
+double prng_probe_store_gbs(uint64_t bytes, int reps);         /* pure 32-B store kernel     */
+double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams); /* host link */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRNG_B200_H */

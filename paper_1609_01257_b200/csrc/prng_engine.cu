@@ -1,0 +1,852 @@
+// prng_engine.cu -- the C ABI of include/prng.h: handle lifecycle, kernel dispatch, the
+// device-only ring, the end-to-end pipeline (device double buffer + side copy stream +
+// pinned host double buffer + sink), interval capture for row a6, built-in sinks and the
+// roofline probes.
+//
+// Paper mapping (§5):
+//   "main thread"  + Main queue  -> s_gen  (generation kernels)
+//   "comms thread" + Comms queue -> s_copy (D2H) + the caller's thread (sink = `out`)
+//   device-side double buffering -> two halves of a device ring of T-iteration batches
+//   semaphores between the threads -> CUDA events (gen(j) -> copy(j); copy(j) -> gen(j+2))
+//   limitation 2 (host-side dual buffer) -> two pinned host halves (mode O2)
+//   limitation 3 (no vectorisation) -> NPT numbers per thread, 32-byte stores
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/prng.h"
+#include "../../include/prng_sinks.h"
+#include "prng_kernels.cuh"
+
+// ============================================================================ errors
+namespace {
+
+int set_err(prng_err_t *err, int code, const char *fmt, ...) {
+    if (err) {
+        err->code = code;
+        va_list ap;
+        va_start(ap, fmt);
+        std::vsnprintf(err->msg, sizeof(err->msg), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+int ok(prng_err_t *err) {
+    if (err) {
+        err->code = PRNG_OK;
+        err->msg[0] = 0;
+    }
+    return PRNG_OK;
+}
+
+#define CU(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess) {                                                                    \
+            if (h) h->poisoned = true;                                                              \
+            return set_err(err, e_ == cudaErrorMemoryAllocation ? PRNG_ENOMEM : PRNG_ECUDA,        \
+                           "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);   \
+        }                                                                                           \
+    } while (0)
+
+// ============================================================================ kernel variants
+using BatchFn = void (*)(prngk::BatchArgs);
+struct Variant {
+    const char *name;
+    int vec, npt, policy;
+    BatchFn fn;
+};
+const Variant kVariants[] = {
+    {"v4n8", 4, 8, 0, prngk::batch_kernel<4, 8, 0>},     // default: 32-B stores, 8 numbers/thread
+    {"v2n4", 2, 4, 0, prngk::batch_kernel<2, 4, 0>},
+    {"v2n8", 2, 8, 0, prngk::batch_kernel<2, 8, 0>},
+    {"v4n4", 4, 4, 0, prngk::batch_kernel<4, 4, 0>},
+    {"v4n16", 4, 16, 0, prngk::batch_kernel<4, 16, 0>},
+    {"v4n8cs", 4, 8, 1, prngk::batch_kernel<4, 8, 1>},
+    {"v2n8cs", 2, 8, 1, prngk::batch_kernel<2, 8, 1>},
+};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+constexpr int kBlock = 256;
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// ============================================================================ the handle
+struct prng {
+    int device = 0;
+    int num_sms = 0;
+    int l2_bytes = 0;
+    uint64_t numrn_total = 0, seed = 0, gid_begin = 0, count = 0;
+    uint64_t pos = 0;  // iterations emitted since prng_init
+    bool inited = false, poisoned = false;
+
+    uint64_t *d_state = nullptr;  // [round_up(count, 4)]
+
+    // device-only ring
+    uint64_t *d_ring = nullptr;
+    uint64_t ring_pitch = 0, ring_slots = 0;
+
+    // end-to-end buffers
+    uint64_t *d_buf = nullptr;  // 2 halves x T slots, pitch buf_pitch
+    uint64_t buf_pitch = 0, buf_T = 0;
+    uint64_t *h_buf[2] = {nullptr, nullptr};
+    bool h_pinned = false;
+    uint64_t h_T = 0;
+    int h_halves = 0;
+
+    cudaStream_t s_gen = nullptr, s_copy = nullptr;
+    bool own_streams = true;
+
+    // options
+    int mode = PRNG_MODE_OVERLAP2;
+    int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0;
+    int profile = 0, kernel = 0;
+    int blocks_per_sm[kNumVariants] = {0};
+
+    // profiling (a6)
+    cudaEvent_t ev_origin = nullptr;
+    double host_origin = 0;
+    struct DevIv {
+        uint32_t name;
+        cudaEvent_t a, b;
+    };
+    std::vector<DevIv> dev_iv;
+    struct HostIv {
+        uint32_t name;
+        double a, b;
+    };
+    std::vector<HostIv> host_iv;
+    double wall_s = 0;
+};
+
+namespace {
+
+uint64_t pitch_for(uint64_t count) { return (count + 3) & ~3ull; }  // 32-byte aligned slots
+
+void free_e2e(prng *h) {
+    if (h->d_buf) cudaFree(h->d_buf);
+    h->d_buf = nullptr;
+    h->buf_T = 0;
+    for (int i = 0; i < 2; ++i) {
+        if (h->h_buf[i]) {
+            if (h->h_pinned)
+                cudaFreeHost(h->h_buf[i]);
+            else
+                std::free(h->h_buf[i]);
+        }
+        h->h_buf[i] = nullptr;
+    }
+    h->h_T = 0;
+    h->h_halves = 0;
+}
+
+void clear_prof(prng *h) {
+    for (auto &iv : h->dev_iv) {
+        cudaEventDestroy(iv.a);
+        cudaEventDestroy(iv.b);
+    }
+    h->dev_iv.clear();
+    h->host_iv.clear();
+    if (h->ev_origin) cudaEventDestroy(h->ev_origin);
+    h->ev_origin = nullptr;
+    h->wall_s = 0;
+}
+
+int ensure_origin(prng *h, prng_err_t *err) {
+    if (!h->profile || h->ev_origin) return PRNG_OK;
+    CU(cudaEventCreate(&h->ev_origin));
+    CU(cudaEventRecord(h->ev_origin, h->s_gen));
+    CU(cudaEventSynchronize(h->ev_origin));
+    h->host_origin = now_s();
+    return PRNG_OK;
+}
+
+// Record-start helper for a profiled device interval on `s`.
+int prof_begin(prng *h, cudaStream_t s, uint32_t name, prng_err_t *err) {
+    if (!h->profile) return PRNG_OK;
+    prng::DevIv iv{name, nullptr, nullptr};
+    CU(cudaEventCreate(&iv.a));
+    CU(cudaEventCreate(&iv.b));
+    CU(cudaEventRecord(iv.a, s));
+    h->dev_iv.push_back(iv);
+    return PRNG_OK;
+}
+int prof_end(prng *h, cudaStream_t s, prng_err_t *err) {
+    if (!h->profile) return PRNG_OK;
+    CU(cudaEventRecord(h->dev_iv.back().b, s));
+    return PRNG_OK;
+}
+
+// Launch one batch of `iters` iterations (a2 + a3) into dst slots.
+int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64_t slot0, uint32_t iters,
+                 bool first_is_state, cudaStream_t s, prng_err_t *err) {
+    const Variant &v = kVariants[h->kernel];
+    prngk::BatchArgs a;
+    a.dst = dst;
+    a.pitch = pitch;
+    a.nslots = (uint32_t)nslots;
+    a.slot0 = (uint32_t)slot0;
+    a.state = h->d_state;
+    a.count = h->count;
+    a.iters = iters;
+    a.first_is_state = first_is_state ? 1u : 0u;
+    const uint64_t piece = 32ull * v.npt;
+    a.npieces = (h->count + piece - 1) / piece;
+    // Persistent grid: at most one wave of resident warps; equalise pieces per warp.
+    uint64_t max_warps = (uint64_t)h->blocks_per_sm[h->kernel] * h->num_sms * (kBlock / 32);
+    if (h->grid_warps > 0) max_warps = std::min<uint64_t>(max_warps, (uint64_t)h->grid_warps);
+    max_warps = std::max<uint64_t>(max_warps, kBlock / 32);
+    const uint64_t rounds0 = (a.npieces + max_warps - 1) / max_warps;
+    const uint64_t warps = (a.npieces + rounds0 - 1) / rounds0;
+    const uint64_t blocks = (warps + kBlock / 32 - 1) / (kBlock / 32);
+    a.rounds = (uint32_t)((a.npieces + blocks * (kBlock / 32) - 1) / (blocks * (kBlock / 32)));
+    if (int rc = prof_begin(h, s, PRNG_EV_RNG_KERNEL, err)) return rc;
+    v.fn<<<(unsigned)blocks, kBlock, 0, s>>>(a);
+    CU(cudaGetLastError());
+    return prof_end(h, s, err);
+}
+
+int check_handle(prng *h, prng_err_t *err, bool need_init) {
+    if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
+    if (h->poisoned) return set_err(err, PRNG_ESTATE, "handle poisoned by an earlier error/abort; call prng_init");
+    if (need_init && !h->inited) return set_err(err, PRNG_ESTATE, "prng_generate before prng_init");
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaSetDevice(%d): %s", h->device, cudaGetErrorString(e));
+    return PRNG_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+const char *prng_strerror(int code) {
+    switch (code) {
+        case PRNG_OK: return "ok";
+        case PRNG_EINVAL: return "invalid argument";
+        case PRNG_ESTATE: return "bad state";
+        case PRNG_ENOMEM: return "out of memory";
+        case PRNG_ECUDA: return "CUDA error";
+        case PRNG_ESINK: return "sink aborted";
+        default: {
+            static thread_local char buf[48];
+            std::snprintf(buf, sizeof(buf), "unknown error %d", code);
+            return buf;
+        }
+    }
+}
+
+const char *prng_event_name(uint32_t id) {
+    static const char *names[PRNG_EV_NAMES] = {"INIT_KERNEL", "RNG_KERNEL", "READ_BUFFER", "OUT"};
+    return id < PRNG_EV_NAMES ? names[id] : "UNKNOWN";
+}
+
+int prng_kernel_variants(void) { return kNumVariants; }
+const char *prng_kernel_variant_name(int id) { return (id >= 0 && id < kNumVariants) ? kVariants[id].name : nullptr; }
+
+prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begin, uint64_t gid_count,
+                          int cuda_device, prng_err_t *err) {
+    // A12: numrn is a cl_uint in the paper: 1 <= numrn <= 2^32.
+    if (numrn_total < 1 || numrn_total > (1ull << 32)) {
+        set_err(err, PRNG_EINVAL, "numrn %llu outside [1, 2^32]", (unsigned long long)numrn_total);
+        return nullptr;
+    }
+    if (gid_count < 1 || gid_begin >= numrn_total || gid_count > numrn_total - gid_begin) {
+        set_err(err, PRNG_EINVAL, "gid range [%llu, +%llu) outside [0, %llu)", (unsigned long long)gid_begin,
+                (unsigned long long)gid_count, (unsigned long long)numrn_total);
+        return nullptr;
+    }
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        set_err(err, PRNG_ECUDA, "no CUDA device: %s", e != cudaSuccess ? cudaGetErrorString(e) : "count 0");
+        return nullptr;
+    }
+    int dev = cuda_device;
+    if (dev < 0) cudaGetDevice(&dev);
+    if (dev >= ndev) {
+        set_err(err, PRNG_EINVAL, "cuda device %d of %d", dev, ndev);
+        return nullptr;
+    }
+    prng *h = new (std::nothrow) prng();
+    if (!h) {
+        set_err(err, PRNG_ENOMEM, "host allocation");
+        return nullptr;
+    }
+    h->device = dev;
+    h->numrn_total = numrn_total;
+    h->seed = seed;
+    h->gid_begin = gid_begin;
+    h->count = gid_count;
+    auto bail = [&](const char *what, cudaError_t ce) -> prng_t * {
+        set_err(err, ce == cudaErrorMemoryAllocation ? PRNG_ENOMEM : PRNG_ECUDA, "%s: %s", what, cudaGetErrorString(ce));
+        prng_destroy(h);
+        return nullptr;
+    };
+    if ((e = cudaSetDevice(dev)) != cudaSuccess) return bail("cudaSetDevice", e);
+    if ((e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+        return bail("cudaDeviceGetAttribute(SMs)", e);
+    cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, dev);
+    for (int i = 0; i < kNumVariants; ++i) {
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm[i], kVariants[i].fn, kBlock, 0)) !=
+            cudaSuccess)
+            return bail("cudaOccupancyMaxActiveBlocksPerMultiprocessor", e);
+        if (h->blocks_per_sm[i] < 1) h->blocks_per_sm[i] = 1;
+    }
+    if ((e = cudaMalloc(&h->d_state, pitch_for(gid_count) * sizeof(uint64_t))) != cudaSuccess)
+        return bail("cudaMalloc(state)", e);
+    if ((e = cudaStreamCreateWithFlags(&h->s_gen, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail("cudaStreamCreate", e);
+    if ((e = cudaStreamCreateWithFlags(&h->s_copy, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail("cudaStreamCreate", e);
+    ok(err);
+    return h;
+}
+
+prng_t *prng_create(uint64_t numrn, uint64_t seed, prng_err_t *err) {
+    return prng_create_range(numrn, seed, 0, numrn, -1, err);
+}
+
+void prng_destroy(prng_t *h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->s_gen) cudaStreamSynchronize(h->s_gen);
+    if (h->s_copy) cudaStreamSynchronize(h->s_copy);
+    clear_prof(h);
+    free_e2e(h);
+    if (h->d_ring) cudaFree(h->d_ring);
+    if (h->d_state) cudaFree(h->d_state);
+    if (h->own_streams) {
+        if (h->s_gen) cudaStreamDestroy(h->s_gen);
+        if (h->s_copy) cudaStreamDestroy(h->s_copy);
+    }
+    delete h;
+}
+
+int prng_set_streams(prng_t *h, void *gen_stream, void *copy_stream, prng_err_t *err) {
+    if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
+    CU(cudaSetDevice(h->device));
+    CU(cudaStreamSynchronize(h->s_gen));
+    CU(cudaStreamSynchronize(h->s_copy));
+    if (h->own_streams) {
+        cudaStreamDestroy(h->s_gen);
+        cudaStreamDestroy(h->s_copy);
+    }
+    h->s_gen = (cudaStream_t)gen_stream;
+    h->s_copy = (cudaStream_t)copy_stream;
+    h->own_streams = false;
+    if (!h->s_gen || !h->s_copy || h->s_gen == h->s_copy)
+        return set_err(err, PRNG_EINVAL, "need two distinct non-NULL streams");
+    return ok(err);
+}
+
+int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
+    if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
+    switch (option) {
+        case PRNG_OPT_MODE:
+            if (value < PRNG_MODE_SERIAL || value > PRNG_MODE_OVERLAP2) return set_err(err, PRNG_EINVAL, "bad mode");
+            if (value != h->mode) free_e2e(h);
+            h->mode = (int)value;
+            break;
+        case PRNG_OPT_BATCH_ITERS:
+            if (value < 0 || value > (1 << 30)) return set_err(err, PRNG_EINVAL, "bad batch iters");
+            if (value != h->batch_iters) free_e2e(h);
+            h->batch_iters = value;
+            break;
+        case PRNG_OPT_RING_SLOTS:
+            if (value < 0 || value > (1 << 30)) return set_err(err, PRNG_EINVAL, "bad ring slots");
+            if (value != h->ring_slots_opt && h->d_ring) {
+                cudaSetDevice(h->device);
+                cudaStreamSynchronize(h->s_gen);
+                cudaFree(h->d_ring);
+                h->d_ring = nullptr;
+                h->ring_slots = 0;
+            }
+            h->ring_slots_opt = value;
+            break;
+        case PRNG_OPT_PROFILE:
+            h->profile = value ? 1 : 0;
+            break;
+        case PRNG_OPT_KERNEL:
+            if (value < 0 || value >= kNumVariants) return set_err(err, PRNG_EINVAL, "bad kernel variant");
+            h->kernel = (int)value;
+            break;
+        case PRNG_OPT_GRID_WARPS:
+            if (value < 0) return set_err(err, PRNG_EINVAL, "bad grid warps");
+            h->grid_warps = value;
+            break;
+        default:
+            return set_err(err, PRNG_EINVAL, "unknown option %d", option);
+    }
+    return ok(err);
+}
+
+int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err) {
+    if (!h || !value) return set_err(err, PRNG_EINVAL, "NULL argument");
+    switch (option) {
+        case PRNG_OPT_MODE: *value = h->mode; break;
+        case PRNG_OPT_BATCH_ITERS: *value = h->batch_iters; break;
+        case PRNG_OPT_RING_SLOTS: *value = h->ring_slots_opt; break;
+        case PRNG_OPT_PROFILE: *value = h->profile; break;
+        case PRNG_OPT_KERNEL: *value = h->kernel; break;
+        case PRNG_OPT_GRID_WARPS: *value = h->grid_warps; break;
+        default: return set_err(err, PRNG_EINVAL, "unknown option %d", option);
+    }
+    return ok(err);
+}
+
+// ---------------------------------------------------------------------------- a1
+int prng_init(prng_t *h, prng_err_t *err) {
+    if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
+    CU(cudaSetDevice(h->device));
+    h->poisoned = false;
+    clear_prof(h);
+    if (int rc = ensure_origin(h, err)) return rc;
+    const double t0 = now_s();
+    prngk::SeedArgs a{h->d_state, h->count, h->gid_begin, h->seed};
+    const uint64_t pairs = (h->count + 1) / 2;
+    const uint64_t max_blocks = (uint64_t)h->num_sms * 8;
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((pairs + kBlock - 1) / kBlock, max_blocks));
+    if (int rc = prof_begin(h, h->s_gen, PRNG_EV_INIT_KERNEL, err)) return rc;
+    prngk::seed_kernel<<<(unsigned)blocks, kBlock, 0, h->s_gen>>>(a);
+    CU(cudaGetLastError());
+    if (int rc = prof_end(h, h->s_gen, err)) return rc;
+    h->pos = 0;
+    h->inited = true;
+    if (h->profile) {
+        CU(cudaStreamSynchronize(h->s_gen));
+        h->wall_s += now_s() - t0;
+    }
+    return ok(err);
+}
+
+// ---------------------------------------------------------------------------- device only
+int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch, uint64_t dst_slots,
+                         void *stream, prng_err_t *err) {
+    if (int rc = check_handle(h, err, true)) return rc;
+    if (numiter < 1) return set_err(err, PRNG_EINVAL, "numiter must be >= 1");
+    if (!dst || ((uintptr_t)dst & 31) || (dst_pitch & 3) || dst_pitch < h->count || dst_slots < 1 ||
+        dst_slots > 0xFFFFFFFFull)
+        return set_err(err, PRNG_EINVAL, "dst must be 32-B aligned, pitch %% 4 == 0, pitch >= count, slots >= 1");
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->s_gen;
+    if (int rc = ensure_origin(h, err)) return rc;
+    uint64_t slot = 0, done = 0;
+    while (done < numiter) {
+        const uint32_t it = (uint32_t)std::min<uint64_t>(numiter - done, 0x7FFFFFFFull);
+        if (int rc = launch_batch(h, dst, dst_pitch, dst_slots, slot, it, h->pos == 0, s, err)) return rc;
+        h->pos += it;
+        done += it;
+        slot = (slot + it) % dst_slots;
+    }
+    return ok(err);
+}
+
+static int ensure_ring(prng *h, uint64_t numiter, prng_err_t *err) {
+    const uint64_t pitch = pitch_for(h->count);
+    uint64_t slots = (uint64_t)h->ring_slots_opt;
+    if (slots == 0) {
+        // >= 16 x L2 bytes (>= 2 GiB on B200) so write-back cannot be absorbed by L2.
+        const uint64_t want = std::max<uint64_t>(16ull * (uint64_t)std::max(h->l2_bytes, 1 << 20), 2ull << 30);
+        slots = std::max<uint64_t>(2, (want + pitch * 8 - 1) / (pitch * 8));
+    }
+    if (h->d_ring && h->ring_slots == slots && h->ring_pitch == pitch) return PRNG_OK;
+    if (h->d_ring) {
+        CU(cudaStreamSynchronize(h->s_gen));
+        cudaFree(h->d_ring);
+        h->d_ring = nullptr;
+    }
+    CU(cudaMalloc(&h->d_ring, slots * pitch * sizeof(uint64_t)));
+    h->ring_slots = slots;
+    h->ring_pitch = pitch;
+    (void)numiter;
+    return PRNG_OK;
+}
+
+static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
+    if (int rc = ensure_ring(h, numiter, err)) return rc;
+    const double t0 = now_s();
+    // Slot of an iteration = iteration mod R, across calls (prng_device_ring documents it).
+    uint64_t done = 0;
+    while (done < numiter) {
+        const uint32_t it = (uint32_t)std::min<uint64_t>(numiter - done, 0x7FFFFFFFull);
+        if (int rc = launch_batch(h, h->d_ring, h->ring_pitch, h->ring_slots, h->pos % h->ring_slots, it,
+                                  h->pos == 0, h->s_gen, err))
+            return rc;
+        h->pos += it;
+        done += it;
+    }
+    CU(cudaStreamSynchronize(h->s_gen));
+    h->wall_s += now_s() - t0;
+    return PRNG_OK;
+}
+
+// ---------------------------------------------------------------------------- end to end
+static int ensure_e2e(prng *h, uint64_t T, int halves, bool pinned, prng_err_t *err) {
+    const uint64_t pitch = pitch_for(h->count);
+    if (!h->d_buf || h->buf_T != T || h->buf_pitch != pitch) {
+        if (h->d_buf) cudaFree(h->d_buf);
+        h->d_buf = nullptr;
+        CU(cudaMalloc(&h->d_buf, 2 * T * pitch * sizeof(uint64_t)));
+        h->buf_T = T;
+        h->buf_pitch = pitch;
+    }
+    if (h->h_T != T || h->h_halves != halves || h->h_pinned != pinned) {
+        for (int i = 0; i < 2; ++i) {
+            if (h->h_buf[i]) h->h_pinned ? (void)cudaFreeHost(h->h_buf[i]) : std::free(h->h_buf[i]);
+            h->h_buf[i] = nullptr;
+        }
+        const size_t bytes = T * h->count * sizeof(uint64_t);
+        for (int i = 0; i < halves; ++i) {
+            if (pinned) {
+                CU(cudaHostAlloc(&h->h_buf[i], bytes, cudaHostAllocDefault));
+            } else {
+                h->h_buf[i] = (uint64_t *)std::malloc(bytes);
+                if (!h->h_buf[i]) return set_err(err, PRNG_ENOMEM, "malloc(%zu)", bytes);
+            }
+        }
+        h->h_T = T;
+        h->h_halves = halves;
+        h->h_pinned = pinned;
+    }
+    return PRNG_OK;
+}
+
+static int enqueue_copy(prng *h, uint64_t *hdst, const uint64_t *dsrc, uint64_t iters, cudaStream_t s,
+                        prng_err_t *err) {
+    if (int rc = prof_begin(h, s, PRNG_EV_READ_BUFFER, err)) return rc;
+    const size_t row = h->count * sizeof(uint64_t);
+    if (h->buf_pitch == h->count) {
+        CU(cudaMemcpyAsync(hdst, dsrc, row * iters, cudaMemcpyDeviceToHost, s));
+    } else {
+        CU(cudaMemcpy2DAsync(hdst, row, dsrc, h->buf_pitch * sizeof(uint64_t), row, iters, cudaMemcpyDeviceToHost, s));
+    }
+    return prof_end(h, s, err);
+}
+
+static int generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void *user, prng_err_t *err) {
+    uint64_t T = (uint64_t)h->batch_iters;
+    const uint64_t row = h->count * sizeof(uint64_t);
+    if (T == 0) T = std::max<uint64_t>(1, (256ull << 20) / row);  // ~256 MiB per batch
+    T = std::min<uint64_t>(T, numiter);
+    const int mode = h->mode;
+    const int halves = (mode == PRNG_MODE_OVERLAP2 || mode == PRNG_MODE_PAGEABLE) ? 2 : 1;
+    if (int rc = ensure_e2e(h, T, halves, mode != PRNG_MODE_PAGEABLE, err)) return rc;
+    const uint64_t nb = (numiter + T - 1) / T;
+    const uint64_t pitch = h->buf_pitch;
+    auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
+    auto dslot = [&](uint64_t j) { return (mode == PRNG_MODE_SERIAL ? 0 : (j & 1)) * T; };
+    const uint64_t pos0 = h->pos;
+    const double t0 = now_s();
+
+    auto run_sink = [&](uint64_t j, const uint64_t *data) -> int {
+        const double a = now_s();
+        int r = sink ? sink(user, pos0 + j * T, iters_of(j), h->gid_begin, h->count, data) : 0;
+        if (h->profile) h->host_iv.push_back({PRNG_EV_OUT, a - h->host_origin, now_s() - h->host_origin});
+        if (r != 0) {
+            h->poisoned = true;
+            return set_err(err, PRNG_ESINK, "sink returned %d at batch %llu", r, (unsigned long long)j);
+        }
+        return PRNG_OK;
+    };
+
+    if (mode == PRNG_MODE_SERIAL) {
+        // S0: everything on one stream, one buffer each side: gen -> read -> out -> gen ...
+        for (uint64_t j = 0; j < nb; ++j) {
+            if (int rc = launch_batch(h, h->d_buf, pitch, 2 * T, 0, iters_of(j), pos0 + j * T == 0, h->s_gen, err))
+                return rc;
+            if (int rc = enqueue_copy(h, h->h_buf[0], h->d_buf, iters_of(j), h->s_gen, err)) return rc;
+            CU(cudaStreamSynchronize(h->s_gen));
+            if (int rc = run_sink(j, h->h_buf[0])) return rc;
+        }
+        h->pos = pos0 + numiter;
+        h->wall_s += now_s() - t0;
+        return PRNG_OK;
+    }
+
+    // Overlapped modes (S1, O1, O2): gen stream + copy stream + events.
+    const int R = 8;  // event ring; at most gen(j+4) / copy(j+2) ahead of the host at batch j
+    cudaEvent_t ev_gen[R], ev_cp[R];
+    for (int i = 0; i < R; ++i) {
+        ev_gen[i] = ev_cp[i] = nullptr;
+    }
+    int rc = PRNG_OK;
+    auto cleanup = [&]() {
+        for (int i = 0; i < R; ++i) {
+            if (ev_gen[i]) cudaEventDestroy(ev_gen[i]);
+            if (ev_cp[i]) cudaEventDestroy(ev_cp[i]);
+        }
+    };
+    for (int i = 0; i < R; ++i) {
+        cudaError_t e1 = cudaEventCreateWithFlags(&ev_gen[i], cudaEventDisableTiming);
+        cudaError_t e2 = cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming);
+        if (e1 != cudaSuccess || e2 != cudaSuccess) {
+            cleanup();
+            h->poisoned = true;
+            return set_err(err, PRNG_ECUDA, "cudaEventCreate failed");
+        }
+    }
+    uint64_t gen_enq = 0, cp_enq = 0;  // batches enqueued so far
+    auto enqueue_gen = [&](uint64_t j) -> int {
+        // gen(j) overwrites device half j%2, last read by copy(j-2)  (WAR, A15)
+        if (j >= 2) {
+            cudaError_t e = cudaStreamWaitEvent(h->s_gen, ev_cp[(j - 2) % R], 0);
+            if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
+        }
+        if (int r = launch_batch(h, h->d_buf, pitch, 2 * T, dslot(j), iters_of(j), pos0 + j * T == 0, h->s_gen, err))
+            return r;
+        cudaError_t e = cudaEventRecord(ev_gen[j % R], h->s_gen);
+        if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaEventRecord: %s", cudaGetErrorString(e));
+        gen_enq = j + 1;
+        return PRNG_OK;
+    };
+    auto enqueue_cp = [&](uint64_t j) -> int {
+        // copy(j) reads device half j%2 after gen(j) wrote it  (RAW, A15)
+        cudaError_t e = cudaStreamWaitEvent(h->s_copy, ev_gen[j % R], 0);
+        if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
+        if (int r = enqueue_copy(h, h->h_buf[j % halves], h->d_buf + dslot(j) * pitch, iters_of(j), h->s_copy, err))
+            return r;
+        e = cudaEventRecord(ev_cp[j % R], h->s_copy);
+        if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaEventRecord: %s", cudaGetErrorString(e));
+        cp_enq = j + 1;
+        return PRNG_OK;
+    };
+
+    // Prologue: gen(0), copy(0), gen(1), [copy(1) if a second host half], gen(2), gen(3).
+    for (uint64_t j = 0; j < std::min<uint64_t>(nb, 2) && !rc; ++j) {
+        rc = enqueue_gen(j);
+        if (!rc && j < (uint64_t)halves) rc = enqueue_cp(j);
+    }
+    while (!rc && gen_enq < nb && gen_enq < cp_enq + 2) rc = enqueue_gen(gen_enq);
+
+    for (uint64_t j = 0; j < nb && !rc; ++j) {
+        cudaError_t e = cudaEventSynchronize(ev_cp[j % R]);
+        if (e != cudaSuccess) {
+            rc = set_err(err, PRNG_ECUDA, "cudaEventSynchronize: %s", cudaGetErrorString(e));
+            break;
+        }
+        rc = run_sink(j, h->h_buf[j % halves]);
+        if (rc) break;
+        // host half j%halves is free again: queue the next copy into it, then the next gen
+        if (cp_enq < nb) rc = enqueue_cp(cp_enq);
+        while (!rc && gen_enq < nb && gen_enq < cp_enq + 2) rc = enqueue_gen(gen_enq);
+    }
+    if (rc) {
+        cudaStreamSynchronize(h->s_gen);
+        cudaStreamSynchronize(h->s_copy);
+        cleanup();
+        h->poisoned = true;
+        return rc;
+    }
+    cudaStreamSynchronize(h->s_gen);
+    cleanup();
+    h->pos = pos0 + numiter;
+    h->wall_s += now_s() - t0;
+    return PRNG_OK;
+}
+
+int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, prng_err_t *err) {
+    if (int rc = check_handle(h, err, true)) return rc;
+    if (numiter < 1) return set_err(err, PRNG_EINVAL, "numiter must be >= 1");
+    if (int rc = ensure_origin(h, err)) return rc;
+    int rc = sink ? generate_e2e(h, numiter, sink, user, err) : generate_device_only(h, numiter, err);
+    if (rc) return rc;
+    return ok(err);
+}
+
+int prng_device_ring(const prng_t *h, uint64_t **base, uint64_t *pitch, uint64_t *slots, uint64_t *last_iter_end,
+                     prng_err_t *err) {
+    if (!h || !base || !pitch || !slots || !last_iter_end) return set_err(err, PRNG_EINVAL, "NULL argument");
+    *base = h->d_ring;
+    *pitch = h->ring_pitch;
+    *slots = h->ring_slots;
+    *last_iter_end = h->pos;
+    return ok(err);
+}
+
+int prng_read_slot(prng_t *h, uint64_t slot, uint64_t *host_dst, prng_err_t *err) {
+    if (int rc = check_handle(h, err, false)) return rc;
+    if (!h->d_ring || slot >= h->ring_slots || !host_dst) return set_err(err, PRNG_EINVAL, "no such ring slot");
+    CU(cudaStreamSynchronize(h->s_gen));
+    CU(cudaMemcpy(host_dst, h->d_ring + slot * h->ring_pitch, h->count * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return ok(err);
+}
+
+int prng_read_state(prng_t *h, uint64_t *host_dst, prng_err_t *err) {
+    if (int rc = check_handle(h, err, false)) return rc;
+    if (!host_dst) return set_err(err, PRNG_EINVAL, "NULL destination");
+    CU(cudaStreamSynchronize(h->s_gen));
+    CU(cudaMemcpy(host_dst, h->d_state, h->count * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return ok(err);
+}
+
+// ---------------------------------------------------------------------------- a6 capture
+int prng_prof_events(const prng_t *hc, uint64_t cap, uint32_t *name_id, double *start_s, double *end_s,
+                     uint64_t *n_out, double *wall_s, prng_err_t *err) {
+    prng *h = const_cast<prng *>(hc);
+    if (!h || !n_out) return set_err(err, PRNG_EINVAL, "NULL argument");
+    const uint64_t n = h->dev_iv.size() + h->host_iv.size();
+    *n_out = n;
+    if (wall_s) *wall_s = h->wall_s;
+    if (cap && (!name_id || !start_s || !end_s)) return set_err(err, PRNG_EINVAL, "NULL output arrays");
+    CU(cudaSetDevice(h->device));
+    uint64_t i = 0;
+    for (const auto &iv : h->dev_iv) {
+        if (i >= cap) break;
+        float a = 0, b = 0;
+        CU(cudaEventSynchronize(iv.b));
+        CU(cudaEventElapsedTime(&a, h->ev_origin, iv.a));
+        CU(cudaEventElapsedTime(&b, h->ev_origin, iv.b));
+        name_id[i] = iv.name;
+        start_s[i] = a * 1e-3;
+        end_s[i] = b * 1e-3;
+        ++i;
+    }
+    for (const auto &iv : h->host_iv) {
+        if (i >= cap) break;
+        name_id[i] = iv.name;
+        start_s[i] = iv.a;
+        end_s[i] = iv.b;
+        ++i;
+    }
+    return ok(err);
+}
+
+// ---------------------------------------------------------------------------- built-in sinks
+int prng_sink_null(void *, uint64_t, uint32_t, uint64_t, uint64_t, const uint64_t *) { return 0; }
+
+int prng_sink_copy(void *user, uint64_t iter_begin, uint32_t iters, uint64_t gid_begin, uint64_t count,
+                   const uint64_t *data) {
+    prng_copy_sink_t *c = (prng_copy_sink_t *)user;
+    for (uint32_t t = 0; t < iters; ++t) {
+        const uint64_t k = iter_begin + t;
+        if (k < c->iter_offset || k - c->iter_offset >= c->iters) return 1;
+        std::memcpy(c->dst + (k - c->iter_offset) * c->dst_pitch + (gid_begin - c->gid_offset), data + t * count,
+                    count * sizeof(uint64_t));
+    }
+    return 0;
+}
+
+int prng_sink_digest(void *user, uint64_t iter_begin, uint32_t iters, uint64_t, uint64_t count,
+                     const uint64_t *data) {
+    prng_digest_sink_t *d = (prng_digest_sink_t *)user;
+    for (uint32_t t = 0; t < iters; ++t) {
+        const uint64_t k = iter_begin + t;
+        if (k < d->iter_offset || k - d->iter_offset >= d->iters) return 1;
+        uint64_t x = 0, s = 0;
+        const uint64_t *row = data + (uint64_t)t * count;
+        for (uint64_t j = 0; j < count; ++j) {
+            x ^= row[j];
+            s += row[j];
+        }
+        d->xor_out[k - d->iter_offset] ^= x;
+        d->sum_out[k - d->iter_offset] += s;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------- probes
+double prng_probe_memset_gbs(uint64_t bytes, int reps) {
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0;
+    cudaMemset(p, 1, bytes);
+    for (int r = 0; r < reps; ++r) {
+        cudaEventRecord(a);
+        cudaMemsetAsync(p, r & 0xff, bytes);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        best = std::max(best, bytes / (ms * 1e-3) / 1e9);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(p);
+    return cudaGetLastError() == cudaSuccess ? best : -1;
+}
+
+double prng_probe_store_gbs(uint64_t bytes, int reps) {
+    uint64_t *p = nullptr;
+    bytes &= ~31ull;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
+    int dev = 0, sms = 0, bps = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, prngk::store_probe_kernel, kBlock, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0;
+    for (int r = 0; r < reps + 1; ++r) {
+        cudaEventRecord(a);
+        prngk::store_probe_kernel<<<sms * std::max(bps, 1), kBlock>>>(p, bytes / 32);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (r) best = std::max(best, bytes / (ms * 1e-3) / 1e9);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(p);
+    return cudaGetLastError() == cudaSuccess ? best : -1;
+}
+
+double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams) {
+    if (nstreams < 1) nstreams = 1;
+    void *d = nullptr, *hbuf = nullptr;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return -1;
+    cudaMemset(d, 7, bytes);
+    if (pinned) {
+        if (cudaHostAlloc(&hbuf, bytes, cudaHostAllocDefault) != cudaSuccess) {
+            cudaFree(d);
+            return -1;
+        }
+    } else {
+        hbuf = std::malloc(bytes);
+        if (!hbuf) {
+            cudaFree(d);
+            return -1;
+        }
+        std::memset(hbuf, 0, bytes);
+    }
+    std::vector<cudaStream_t> ss(nstreams);
+    for (auto &s : ss) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    double best = 0;
+    const uint64_t chunk = (bytes / nstreams) & ~4095ull;
+    for (int r = 0; r < reps + 1; ++r) {
+        cudaDeviceSynchronize();
+        const double t0 = now_s();
+        for (int i = 0; i < nstreams; ++i) {
+            const uint64_t off = i * chunk, len = (i == nstreams - 1) ? bytes - off : chunk;
+            cudaMemcpyAsync((char *)hbuf + off, (char *)d + off, len, cudaMemcpyDeviceToHost, ss[i]);
+        }
+        for (auto &s : ss) cudaStreamSynchronize(s);
+        const double dt = now_s() - t0;
+        if (r) best = std::max(best, bytes / dt / 1e9);
+    }
+    for (auto &s : ss) cudaStreamDestroy(s);
+    if (pinned)
+        cudaFreeHost(hbuf);
+    else
+        std::free(hbuf);
+    cudaFree(d);
+    return cudaGetLastError() == cudaSuccess ? best : -1;
+}
+
+}  // extern "C"

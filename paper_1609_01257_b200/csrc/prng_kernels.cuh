@@ -1,0 +1,227 @@
+// prng_kernels.cuh -- sm_100a kernels of the massive-PRNG hot path (arXiv 1609.01257 §5).
+//
+//   a1  seed_kernel   : state[g] = seed64(gid_begin + g, seed)          (readings A1-A4)
+//   a2+a3 batch_kernel: T iterations of xorshift64 per launch, state held in registers,
+//                       every iteration stored with 32-byte (or 16-byte) coalesced vector
+//                       stores into a ring of iteration slots            (A5-A8)
+//
+// The paper's OpenCL `prng` kernel re-reads its state from one buffer and writes the
+// successor to another every iteration (16 B/number of global traffic).
+// Here a persistent grid-strided warp owns a "piece" of 32*NPT consecutive gids, keeps
+// its NPT states in registers for all T iterations of the launch and only writes
+// (8 B/number); the state array is read once and written once per launch.
+//
+// Work decomposition:
+//   piece p covers gids [p*32*NPT, (p+1)*32*NPT) of the handle's range;
+//   lane l holds, for v in 0..NPT/VEC-1, the VEC consecutive gids at
+//   p*32*NPT + v*32*VEC + l*VEC  -> one warp-wide store instruction writes 32*VEC*8
+//   contiguous bytes (512 B for VEC = 2, 1 KiB for VEC = 4).
+//   warp w of W processes pieces w, w+W, w+2W, ... (`rounds` of them); the host sizes W so
+//   that every warp gets the same number of pieces +- 1 and the grid is <= one wave.
+//
+// No code here is shared with oracle/ (the CPU definition); see DESIGN.md §2.
+#pragma once
+#include <cstdint>
+
+namespace prngk {
+
+// ---------------------------------------------------------------- the method's arithmetic
+// A1: Wang's 32-bit multiplicative hash ("hash32shiftmult"), P:173 [wang1997inthash].
+__device__ __forceinline__ uint32_t wang32(uint32_t x) {
+    x = (x ^ 61u) ^ (x >> 16);
+    x = x * 9u;
+    x = x ^ (x >> 4);
+    x = x * 0x27d4eb2du;
+    x = x ^ (x >> 15);
+    return x;
+}
+
+// A4: seed premix (the paper has no seed; fmix64(0) == 0 keeps seed 0 == the paper).
+__device__ __forceinline__ uint64_t premix64(uint64_t z) {
+    z ^= z >> 33;
+    z *= 0xff51afd7ed558ccdull;
+    z ^= z >> 33;
+    z *= 0xc4ceb9fe1a85ec53ull;
+    z ^= z >> 33;
+    return z;
+}
+
+// A2/A3: two 32-bit hashes of the 32-bit gid composed into the 64-bit state; 0 -> 1.
+__device__ __forceinline__ uint64_t seed64(uint32_t g, uint32_t key_hi, uint32_t key_lo) {
+    const uint64_t st = ((uint64_t)wang32(g ^ key_hi) << 32) | (uint64_t)wang32(g ^ 0x9E3779B9u ^ key_lo);
+    return st ? st : 1ull;
+}
+
+// A5: Marsaglia's xor64 triple (13, 7, 17), P:177 [marsaglia2003xorshift].
+__device__ __forceinline__ uint64_t xorshift64(uint64_t x) {
+    x ^= x << 13;
+    x ^= x >> 7;
+    x ^= x << 17;
+    return x;
+}
+
+// ---------------------------------------------------------------- vector memory helpers
+// POLICY 0: default write-back; 1: .cs (streaming, evict-first) -- the output is never
+// re-read by the SMs, only by the copy engine.
+template <int POLICY>
+__device__ __forceinline__ void st_v4(uint64_t *p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+    if constexpr (POLICY == 1)
+        asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+    else
+        asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+template <int POLICY>
+__device__ __forceinline__ void st_v2(uint64_t *p, uint64_t a, uint64_t b) {
+    if constexpr (POLICY == 1)
+        asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+    else
+        asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_v4(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
+    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+__device__ __forceinline__ void ld_v2(const uint64_t *p, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+
+template <int VEC, int POLICY>
+__device__ __forceinline__ void store_vec(uint64_t *p, const uint64_t *x) {
+    if constexpr (VEC == 4)
+        st_v4<POLICY>(p, x[0], x[1], x[2], x[3]);
+    else
+        st_v2<POLICY>(p, x[0], x[1]);
+}
+template <int VEC>
+__device__ __forceinline__ void load_vec(const uint64_t *p, uint64_t *x) {
+    if constexpr (VEC == 4)
+        ld_v4(p, x[0], x[1], x[2], x[3]);
+    else
+        ld_v2(p, x[0], x[1]);
+}
+
+// ---------------------------------------------------------------- a1: seed kernel
+struct SeedArgs {
+    uint64_t *state;     // [count] out, 16-byte aligned
+    uint64_t count;      // gids in this handle's range
+    uint64_t gid_begin;  // first global gid (< 2^32)
+    uint64_t seed;
+};
+
+// Each thread seeds 2 consecutive gids per grid-stride step and writes them with one
+// 16-byte store.
+__global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
+    const uint64_t m = premix64(a.seed);
+    const uint32_t key_hi = (uint32_t)m, key_lo = (uint32_t)(m >> 32);
+    const uint64_t stride = 2ull * gridDim.x * blockDim.x;
+    for (uint64_t i = 2ull * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x); i < a.count; i += stride) {
+        const uint32_t g = (uint32_t)(a.gid_begin + i);
+        const uint64_t s0 = seed64(g, key_hi, key_lo);
+        if (i + 1 < a.count) {
+            const uint64_t s1 = seed64(g + 1u, key_hi, key_lo);
+            st_v2<0>(a.state + i, s0, s1);
+        } else {
+            a.state[i] = s0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- a2+a3: batch kernel
+struct BatchArgs {
+    uint64_t *dst;            // slot s starts at dst + s * pitch (32-byte aligned)
+    uint64_t pitch;           // u64 elements between slots (multiple of 4, >= count)
+    uint32_t nslots;          // ring slots R (iteration t of the launch -> slot (slot0 + t) mod R)
+    uint32_t slot0;           // slot of the launch's first iteration
+    uint64_t *state;          // [count] in/out: state before / after the launch
+    uint64_t count;           // gids in the handle's range
+    uint32_t iters;           // T iterations in this launch
+    uint32_t first_is_state;  // 1: the launch's first iteration is iteration 0 (= the seeds):
+                              //    emit the state unchanged, then step (A6)
+    uint64_t npieces;         // ceil(count / (32 * NPT))
+    uint32_t rounds;          // ceil(npieces / warps in grid)
+};
+
+template <int VEC, int NPT, int POLICY, bool FULL>
+__device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base) {
+    constexpr int NV = NPT / VEC;
+    uint64_t x[NPT];
+    // ---- load the NPT states of this lane (read once per launch)
+    if constexpr (FULL) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+    } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const uint64_t idx = base + (uint64_t)v * 32 * VEC + e;
+                x[v * VEC + e] = idx < a.count ? a.state[idx] : 0ull;
+            }
+    }
+    uint64_t *p = a.dst + (uint64_t)a.slot0 * a.pitch + base;
+    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
+    uint32_t slot = a.slot0;
+    for (uint32_t t = 0; t < a.iters; ++t) {
+        if (t > 0 || !a.first_is_state) {
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
+        }
+        if constexpr (FULL) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) store_vec<VEC, POLICY>(p + v * 32 * VEC, x + v * VEC);
+        } else {
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    if (base + (uint64_t)v * 32 * VEC + e < a.count) p[v * 32 * VEC + e] = x[v * VEC + e];
+        }
+        // advance to the next slot of the ring (warp-uniform)
+        if (++slot == a.nslots) {
+            slot = 0;
+            p -= wrap;
+        } else {
+            p += a.pitch;
+        }
+    }
+    // ---- write the state back (== the launch's last iteration)
+    if constexpr (FULL) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+    } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const uint64_t idx = base + (uint64_t)v * 32 * VEC + e;
+                if (idx < a.count) a.state[idx] = x[v * VEC + e];
+            }
+    }
+}
+
+template <int VEC, int NPT, int POLICY>
+__global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
+    static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
+    constexpr uint64_t PIECE = 32ull * NPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint32_t r = 0; r < a.rounds; ++r) {
+        const uint64_t piece = (uint64_t)r * nwarps + warp;
+        if (piece >= a.npieces) break;  // warp-uniform
+        const uint64_t base = piece * PIECE + (uint64_t)lane * VEC;
+        if ((piece + 1) * PIECE <= a.count)
+            run_piece<VEC, NPT, POLICY, true>(a, base);
+        else
+            run_piece<VEC, NPT, POLICY, false>(a, base);
+    }
+}
+
+// ---------------------------------------------------------------- roofline probe kernel
+// Pure 32-byte streaming store of a constant pattern: the same-box write ceiling.
+__global__ void __launch_bounds__(256) store_probe_kernel(uint64_t *p, uint64_t n4) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride)
+        st_v4<0>(p + 4 * i, i, i + 1, i + 2, i + 3);
+}
+
+}  // namespace prngk

@@ -1,0 +1,134 @@
+"""CPU-side checks of the C-ABI library (no GPU compute calls): it builds, loads, exports
+every symbol include/*.h declares, validates arguments, fails loudly without a GPU, and its
+host-side profiler arithmetic (row a6) matches oracle/prof.py."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1609_01257_b200 as P
+from oracle import prof as oprof
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    names = set()
+    for h in ("prng.h", "prng_sinks.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(prng_\w+)\s*\(", src, flags=re.M):
+            names.add(m.group(1))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    P.lib()
+    declared = _declared_functions()
+    assert {"prng_create", "prng_init", "prng_generate", "prng_destroy", "prng_strerror",
+            "prng_create_range", "prng_prof_calc", "prng_sink_null"} <= declared
+    out = subprocess.run(["nm", "-D", "--defined-only", P.LIB], capture_output=True, text=True, check=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if l.strip()}
+    missing = declared - exported
+    assert not missing, f"declared in include/ but not exported: {missing}"
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", P.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_strerror_total():
+    assert P.prng_strerror(0) == "ok"
+    assert P.prng_strerror(-5) == "sink aborted"
+    assert P.prng_strerror(12345) == "unknown error 12345"
+
+
+def test_create_validates_before_touching_the_device():
+    for args in [(0, 0), ((1 << 32) + 1, 0)]:
+        with pytest.raises(P.PrngError) as e:
+            P.prng_create(*args)
+        assert e.value.code == P.PRNG_EINVAL
+    with pytest.raises(P.PrngError) as e:
+        P.prng_create_range(100, 0, 90, 20)
+    assert e.value.code == P.PRNG_EINVAL
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(P.PrngError) as e:
+        P.prng_create(1024)
+    assert e.value.code == P.PRNG_ECUDA
+
+
+def test_null_handle_calls_fail_cleanly():
+    err = P.prng_err_t()
+    assert P.lib().prng_init(None, ctypes.byref(err)) == P.PRNG_EINVAL
+    assert P.lib().prng_generate(None, 4, None, None, ctypes.byref(err)) == P.PRNG_EINVAL
+    P.prng_destroy(None)  # NULL-safe
+
+
+def test_variants_named():
+    n = P.prng_kernel_variants()
+    names = [P.prng_kernel_variant_name(i) for i in range(n)]
+    assert names[0] == "v4n8" and len(set(names)) == n
+    assert P.prng_kernel_variant_name(n) is None
+    assert [P.prng_event_name(i) for i in range(4)] == list(P.EV_NAMES)
+
+
+# ---------------------------------------------------------------- a6: profiler arithmetic
+def _compare(events, elapsed=None):
+    names = sorted({n for n, _, _ in events}) or ["A"]
+    idx = {n: i for i, n in enumerate(names)}
+    ids = [idx[n] for n, _, _ in events]
+    r = P.prng_prof_calc(ids, [s for _, s, _ in events], [e for _, _, e in events], len(names),
+                         elapsed or 0.0)
+    o = oprof.report(events, elapsed=elapsed)
+    for n, (a, _) in o["aggregate"].items():
+        assert r["agg"][idx[n]] == pytest.approx(a, abs=1e-9)
+    for (a, b), v in o["overlaps"].items():
+        i, j = sorted((idx[a], idx[b]))
+        assert r["overlap"][i, j] == pytest.approx(v, abs=1e-9)
+    tot_ov = sum(o["overlaps"].values())
+    assert np.triu(r["overlap"]).sum() == pytest.approx(tot_ov, abs=1e-9)
+    assert r["effective"] == pytest.approx(o["effective"], abs=1e-9)
+    if events:
+        assert r["elapsed"] == pytest.approx(o["elapsed"], abs=1e-12)
+
+
+def test_prof_calc_matches_oracle_random():
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        m = int(rng.integers(0, 12))
+        ev = []
+        for _ in range(m):
+            s = int(rng.integers(0, 80))
+            ev.append((str(rng.choice(["INIT_KERNEL", "RNG_KERNEL", "READ_BUFFER", "OUT"])), s,
+                       s + int(rng.integers(0, 30))))
+        _compare(ev)
+
+
+def test_prof_calc_fig3(golden):
+    """The Fig. 3 timeline through the C++ arithmetic."""
+    g = golden("fig3_profile_summary.json")
+    rng, read, init = (g["aggregate_abs_s"][k] for k in ("RNG_KERNEL", "READ_BUFFER", "INIT_KERNEL"))
+    ov = g["overlap_total_s"]
+    ids = [0, 2, 1]
+    s = [0.0, 1.0, 1.0 + read - ov]
+    e = [init, 1.0 + read, 1.0 + read - ov + rng]
+    r = P.prng_prof_calc(ids, s, e, 4, g["elapsed_s"])
+    assert r["overlap"][1, 2] == pytest.approx(ov, rel=1e-9)
+    assert r["effective"] == pytest.approx(g["effective_s"], rel=5e-6)
+    assert round(100 * r["effective"] / r["elapsed"], 2) == g["device_pct"]
+
+
+def test_prof_calc_rejects_bad_input():
+    with pytest.raises(P.PrngError):
+        P.prng_prof_calc([5], [0.0], [1.0], 4)
+    with pytest.raises(P.PrngError):
+        P.prng_prof_calc([0], [2.0], [1.0], 4)

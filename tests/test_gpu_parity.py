@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+bit-exact (integer work, BASELINE.json north_star).  Every test here needs a B200."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1609_01257_b200 as P
+from workloads import RAGGED_N, SEED_PARITY, SPEC_GRID_I, SPEC_GRID_N, sample_points, shard_range
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.init()
+    yield
+
+
+def run_e2e(numrn, numiter, seed=0, mode=P.PRNG_MODE_OVERLAP2, batch=0, kernel=0, gid_begin=0, count=None,
+            calls=None, profile=False):
+    """Generate through prng_generate with the copy sink; returns [numiter, count] uint64."""
+    count = numrn - gid_begin if count is None else count
+    h = P.prng_create_range(numrn, seed, gid_begin, count)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_MODE, mode)
+        P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, batch)
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, kernel)
+        P.prng_set_option(h, P.PRNG_OPT_PROFILE, int(profile))
+        out = np.full((numiter, count), 0xDEADBEEF, dtype=np.uint64)
+        sink = P.CopySink(out.ctypes.data_as(P.P64), count, 0, numiter, gid_begin)
+        P.prng_init(h)
+        for c in (calls or [numiter]):
+            P.prng_generate(h, c, P.SINK_COPY, sink)
+        prof = P.prng_prof_events(h) if profile else None
+        st = P.prng_read_state(h, count)
+    finally:
+        P.prng_destroy(h)
+    assert np.array_equal(st, out[-1]), "state after generate must equal the last emitted iteration"
+    return (out, prof) if profile else out
+
+
+# ---------------------------------------------------------------- config 1 and golden digests
+@pytest.mark.parametrize("seed", [0, 1, SEED_PARITY])
+def test_config1_bit_exact(seed, golden):
+    """BASELINE config 1: n = 1024, i = 8 vs the oracle, plus SURVEY App. A digests."""
+    out = run_e2e(1024, 8, seed)
+    assert np.array_equal(out, oracle.stream(1024, 8, seed))
+    d = golden("survey_appendix_a.json")["config1_n1024_i8"][str(seed)]
+    assert hashlib.sha256(out.astype("<u8").tobytes()).hexdigest() == d["sha256"]
+
+
+def test_n1_i1_bytes(golden):
+    out = run_e2e(1, 1)
+    assert out.astype("<u8").tobytes().hex() == golden("spec_examples.json")["n1_i1_stream_hex"]
+
+
+@pytest.mark.parametrize("n", SPEC_GRID_N)
+@pytest.mark.parametrize("i", SPEC_GRID_I)
+def test_spec_grid(n, i):
+    """S:499 / S:582 grid, with small batches so ring halves wrap (T = 3 does not divide i)."""
+    assert np.array_equal(run_e2e(n, i, SEED_PARITY, batch=3), oracle.stream(n, i, SEED_PARITY))
+
+
+@pytest.mark.parametrize("n", RAGGED_N)
+def test_ragged_sizes_all_variants(n):
+    """Sizes that split pieces, vectors and warps raggedly, for every kernel variant."""
+    want = oracle.stream(n, 5, 7)
+    for kv in range(P.prng_kernel_variants()):
+        got = run_e2e(n, 5, 7, batch=2, kernel=kv)
+        assert np.array_equal(got, want), f"variant {P.prng_kernel_variant_name(kv)}"
+
+
+@pytest.mark.parametrize("mode", [P.PRNG_MODE_SERIAL, P.PRNG_MODE_PAGEABLE, P.PRNG_MODE_OVERLAP1,
+                                  P.PRNG_MODE_OVERLAP2])
+@pytest.mark.parametrize("batch", [0, 1, 3, 7])
+def test_pipeline_modes(mode, batch):
+    n, i = 5000, 16
+    assert np.array_equal(run_e2e(n, i, 11, mode=mode, batch=batch), oracle.stream(n, i, 11))
+
+
+def test_split_call_equivalence():
+    """A10: generate(3); generate(5) == generate(8); and generate(1) x 8."""
+    want = oracle.stream(3000, 8, 4)
+    assert np.array_equal(run_e2e(3000, 8, 4, calls=[3, 5], batch=2), want)
+    assert np.array_equal(run_e2e(3000, 8, 4, calls=[1] * 8), want)
+
+
+def test_sharding_reassembles():
+    """A11: rank shards of the global gid space reassemble to the single-range stream."""
+    n, i = 10007, 6
+    want = oracle.stream(n, i, SEED_PARITY)
+    for world in (2, 3, 4, 8):
+        parts = [run_e2e(n, i, SEED_PARITY, gid_begin=b, count=c)
+                 for b, c in (shard_range(n, r, world) for r in range(world))]
+        assert np.array_equal(np.concatenate(parts, axis=1), want)
+
+
+def test_top_of_gid_range():
+    """numrn = 2^32 (the maximum, A12): the last 1000 gids, up to gid 2^32 - 1."""
+    n = 1 << 32
+    got = run_e2e(n, 4, 3, gid_begin=n - 1000, count=1000)
+    assert np.array_equal(got, oracle.stream(n, 4, 3, gid_begin=n - 1000, count=1000))
+
+
+def test_mid_size_full_compare():
+    """Several full waves of the persistent grid plus a ragged tail, full compare."""
+    n, i = (1 << 20) + 13, 12
+    assert np.array_equal(run_e2e(n, i, SEED_PARITY, batch=5), oracle.stream(n, i, SEED_PARITY))
+
+
+# ---------------------------------------------------------------- device-only path
+def test_device_only_into_torch_tensor():
+    import torch
+    n, i = 70001, 9
+    pitch = (n + 3) // 4 * 4
+    buf = torch.zeros((i, pitch), dtype=torch.int64, device="cuda")
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_init(h)
+        P.prng_generate_device(h, i, buf.data_ptr(), pitch, i, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+    finally:
+        P.prng_destroy(h)
+    got = buf[:, :n].cpu().numpy().view(np.uint64)
+    assert np.array_equal(got, oracle.stream(n, i, SEED_PARITY))
+
+
+def test_device_only_ring_wraps():
+    """Ring of R = 3 slots, 8 iterations in two calls: slots hold iterations 5, 6, 7."""
+    n = 4099
+    h = P.prng_create(n, 2)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, 3)
+        P.prng_init(h)
+        P.prng_generate(h, 3)
+        P.prng_generate(h, 5)
+        base, pitch, slots, end = P.prng_device_ring(h)
+        assert slots == 3 and end == 8
+        want = oracle.stream(n, 8, 2)
+        for k in range(5, 8):
+            assert np.array_equal(P.prng_read_slot(h, k % slots, n), want[k])
+        assert np.array_equal(P.prng_read_state(h, n), want[7])
+    finally:
+        P.prng_destroy(h)
+
+
+@pytest.mark.slow
+def test_full_size_config2_sampled():
+    """BASELINE config 2 in bench.py's launch configuration (n = 2^24, numiter = 1000,
+    device only, default variant and ring): every output of the last ring slots at sampled
+    gids, and the final state at sampled gids, vs the oracle's random-access form."""
+    n, i = 1 << 24, 1000
+    h = P.prng_create(n, 0)
+    try:
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        _, pitch, slots, end = P.prng_device_ring(h)
+        g, k = sample_points(n, i, 2000, rng_seed=99)
+        st = P.prng_read_state(h, n)
+        for gg in g[:500]:
+            assert int(st[gg]) == oracle.sample(int(gg), i - 1, 0)
+        for kk in sorted({i - 1, i - slots, i - slots // 2}):
+            row = P.prng_read_slot(h, kk % slots, n)
+            for gg in g[:300]:
+                assert int(row[gg]) == oracle.sample(int(gg), kk, 0)
+        # one whole slot: every gid at the last iteration equals the state
+        assert np.array_equal(P.prng_read_slot(h, (i - 1) % slots, n), st)
+    finally:
+        P.prng_destroy(h)
+
+
+@pytest.mark.slow
+def test_full_width_e2e_digests():
+    """Config 3's width (n = 2^24) end to end with per-iteration XOR / sum digests over every
+    output (numiter cut to 24 so the single-threaded oracle finishes in seconds)."""
+    n, i = 1 << 24, 24
+    xo = np.zeros(i, np.uint64)
+    so = np.zeros(i, np.uint64)
+    d = P.DigestSink(xo.ctypes.data_as(P.P64), so.ctypes.data_as(P.P64), 0, i)
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_init(h)
+        P.prng_generate(h, i, P.SINK_DIGEST, d)
+    finally:
+        P.prng_destroy(h)
+    wx, ws = oracle.digest(n, i, SEED_PARITY)
+    assert np.array_equal(xo, wx) and np.array_equal(so, ws)
+
+
+# ---------------------------------------------------------------- errors and causality
+def test_state_errors():
+    h = P.prng_create(100, 0)
+    try:
+        with pytest.raises(P.PrngError) as e:
+            P.prng_generate(h, 1)
+        assert e.value.code == P.PRNG_ESTATE
+        P.prng_init(h)
+        with pytest.raises(P.PrngError) as e:
+            P.prng_generate(h, 0)
+        assert e.value.code == P.PRNG_EINVAL
+        with pytest.raises(P.PrngError) as e:
+            P.prng_generate(h, 10, lambda *a: 1)   # sink aborts
+        assert e.value.code == P.PRNG_ESINK
+        with pytest.raises(P.PrngError) as e:
+            P.prng_generate(h, 1, P.SINK_NULL)
+        assert e.value.code == P.PRNG_ESTATE      # poisoned until re-init
+        P.prng_init(h)
+        P.prng_generate(h, 2, P.SINK_NULL)
+    finally:
+        P.prng_destroy(h)
+
+
+def test_python_sink_sees_ordered_batches():
+    seen = []
+    h = P.prng_create(333, 5)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 2)
+        P.prng_init(h)
+        P.prng_generate(h, 7, lambda k0, it, g0, cnt, arr: seen.append((k0, it, g0, cnt, arr.copy())) and 0)
+    finally:
+        P.prng_destroy(h)
+    assert [(s[0], s[1]) for s in seen] == [(0, 2), (2, 2), (4, 2), (6, 1)]
+    assert np.array_equal(np.concatenate([s[4] for s in seen]), oracle.stream(333, 7, 5))
+
+
+@pytest.mark.parametrize("mode", [P.PRNG_MODE_OVERLAP1, P.PRNG_MODE_OVERLAP2])
+def test_profile_causality(mode):
+    """S:501 causality on the recorded intervals: READ_j starts after RNG_j ends; RNG_{j+2}
+    (which overwrites RNG_j's device half) starts after READ_j ends; counts per S:496."""
+    n, i, T = 1 << 16, 12, 2
+    out, (ids, s, e, wall) = run_e2e(n, i, 3, mode=mode, batch=T, profile=True)
+    assert np.array_equal(out, oracle.stream(n, i, 3))
+    nb = i // T
+    rng = [(a, b) for n_, a, b in zip(ids, s, e) if n_ == 1]
+    rd = [(a, b) for n_, a, b in zip(ids, s, e) if n_ == 2]
+    outs = [(a, b) for n_, a, b in zip(ids, s, e) if n_ == 3]
+    assert (ids == 0).sum() == 1 and len(rng) == nb and len(rd) == nb and len(outs) == nb
+    eps = 2e-6
+    for j in range(nb):
+        assert rd[j][0] >= rng[j][1] - eps
+        if j + 2 < nb:
+            assert rng[j + 2][0] >= rd[j][1] - eps
+    assert wall > 0

@@ -1,0 +1,19 @@
+#!/bin/bash
+# One gpurun call: build, GPU tests, smoke, bench, ncu launch list + full capture of the top kernel.
+# Usage (from the repo root, on the GPU box): bash tools/gpu_check.sh [tag]
+set -x
+TAG=${1:-r1}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+nvidia-smi topo -m > $OUT/topo.txt 2>&1
+lscpu > $OUT/lscpu.txt 2>&1; nproc >> $OUT/lscpu.txt; free -g >> $OUT/lscpu.txt
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-probes > $OUT/ncu_launches.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:batch_kernel -s 1 -c 1 \
+    -o $OUT/prof_batch python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-probes > $OUT/ncu_full.log 2>&1
+ls -la $OUT
