@@ -31,7 +31,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -55,7 +54,7 @@ def parse():
     ap.add_argument("--numrn-total", type=int, default=0, help="strong scaling: fixed total numrn (e.g. 2^28)")
     ap.add_argument("--numiter", type=int, default=DEF_NUMITER)
     ap.add_argument("--seed", type=int, default=SEED_PERF)
-    ap.add_argument("--kernel", type=int, default=0, help="kernel variant id")
+    ap.add_argument("--kernel", type=int, default=-1, help="kernel variant id (-1: prng_autotune picks)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--e2e-mode", type=int, default=3, help="0 S0, 1 S1, 2 O1, 3 O2")
@@ -100,53 +99,62 @@ class Dist:
 
 # ---------------------------------------------------------------- clocks during timing
 class Clocks:
-    """nvidia-smi sampled every 100 ms while the timed region runs (B200_PROFILING.md)."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + clock-event reasons sampled every 5 ms by NVML (nvidia_ml_py) in a thread
+    while the timed region runs (B200_PROFILING.md's clocks line; nvidia-smi would need
+    ~0.5 s to start, longer than the ~100 ms device-only timed region).  Samples taken
+    while the GPU is idle (GpuIdle reason) are excluded from the median."""
 
     def __init__(self, index):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.rows.append(self._sample())
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+    def _sample(self):
+        N = self.N
+        return (N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM), N.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+
+    def _loop(self):
+        while not self.stop.is_set():
+            try:
+                self.rows.append(self._sample())
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop.wait(0.005)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
             self.t.join(timeout=2)
+            self.rows.append(self._sample())
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for i, nm in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        if not self.t:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: " + getattr(self, "err", "")]}
+        N = self.N
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap,
+                "hw_power_brake_slowdown": N.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        busy = [(c, r) for c, r in self.rows if not (r & N.nvmlClocksEventReasonGpuIdle)] or self.rows
+        reasons = sorted({nm for _, r in busy for nm, b in bits.items() if r & b})
+        return {"sm_mhz": statistics.median(c for c, _ in busy), "sm_max_mhz": self.max, "reasons": reasons,
+                "samples": len(self.rows), "busy_samples": len(busy), "source": "nvml 5 ms"}
 
 
 def measured_peaks():
@@ -216,8 +224,14 @@ def run_ours(a, D):
     cop = torch.cuda.Stream()
     h = P.prng_create_range(numrn, a.seed, gb, cnt, D.local)
     P.prng_set_streams(h, gen.cuda_stream, cop.cuda_stream)
-    P.prng_set_option(h, P.PRNG_OPT_KERNEL, a.kernel)
     P.prng_set_option(h, P.PRNG_OPT_MODE, a.e2e_mode)
+    tune_gbs = None
+    if a.kernel < 0:  # untimed setup, like a library autotuner
+        tune_gbs = P.prng_autotune(h)
+    else:
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, a.kernel)
+    kernel = P.prng_get_option(h, P.PRNG_OPT_KERNEL)
+    grid_warps = P.prng_get_option(h, P.PRNG_OPT_GRID_WARPS)
 
     # ---- device only
     for _ in range(a.warmup):
@@ -253,7 +267,8 @@ def run_ours(a, D):
     achieved = algo_bytes / (kmean * 1e-3) / 1e9
     traffic, _ = ncu_traffic()
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "prngk::batch_kernel<" + P.prng_kernel_variant_name(a.kernel) + ">",
+                "traffic": traffic, "kernel": "prngk::batch_kernel<" + P.prng_kernel_variant_name(kernel) + ">",
+                "grid_warps": grid_warps or "variant default", "autotune_probe_gbs": tune_gbs,
                 "algorithmic_bytes_per_launch": algo_bytes, "mean_launch_ms": kmean,
                 "kernel_share_of_step": sum(kern_ms) / ms, "init_kernel_mean_ms": statistics.mean(init_ms),
                 "peak_source": peak_src}

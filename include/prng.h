@@ -130,7 +130,9 @@ enum prng_option {
     PRNG_OPT_RING_SLOTS = 3,   /* R of the device-only ring; 0 = auto (>= 16x L2 bytes)   */
     PRNG_OPT_PROFILE = 4,      /* 1 = record per-batch intervals (CUDA events)           */
     PRNG_OPT_KERNEL = 5,       /* kernel variant id (see prng_kernel_variants); 0 = default */
-    PRNG_OPT_GRID_WARPS = 6    /* cap on resident warps of the persistent grid; 0 = auto  */
+    PRNG_OPT_GRID_WARPS = 6,   /* cap on resident warps of the persistent grid; 0 = auto  */
+    PRNG_OPT_RING_PAD = 7      /* extra u64 elements between device-only ring slots (multiple
+                                  of 4; breaks power-of-two slot strides); default 0       */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two
@@ -146,8 +148,16 @@ enum prng_mode {
 int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err);
 int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err);
 
-/* Number of kernel variants compiled in, and the name of one ("v4n8" = 32-byte stores,
- * 8 numbers per thread). */
+/* Measure a short list of (kernel variant, warps per SM) candidates on this handle's
+ * device-only ring (probe_iters iterations each, 0 = auto: ~16 GiB of output) and keep
+ * the fastest as PRNG_OPT_KERNEL + PRNG_OPT_GRID_WARPS.  The probes consume the device
+ * state, so the handle must be prng_init'ed again afterwards (generate returns
+ * PRNG_ESTATE otherwise).  best_gbs (may be NULL) gets the winner's probe GB/s. */
+int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err);
+
+/* Number of kernel variants compiled in, and the name of one ("v2n4s1" = 16-byte stores,
+ * 4 numbers per thread, CTA barrier every iteration; "v4n8" = 32-byte stores, 8 numbers
+ * per thread, free-running warps). */
 int prng_kernel_variants(void);
 const char *prng_kernel_variant_name(int id);
 

@@ -19,18 +19,18 @@ __all__ = [
     "prng_generate", "prng_generate_device", "prng_device_ring", "prng_read_slot",
     "prng_read_state", "prng_set_option", "prng_get_option", "prng_set_streams",
     "prng_strerror", "prng_prof_events", "prng_prof_calc", "prng_event_name",
-    "prng_kernel_variants", "prng_kernel_variant_name", "prng_probe_memset_gbs",
+    "prng_kernel_variants", "prng_kernel_variant_name", "prng_autotune", "prng_probe_memset_gbs",
     "prng_probe_store_gbs", "prng_probe_d2h_gbs", "SINK_NULL", "SINK_COPY", "SINK_DIGEST",
     "CopySink", "DigestSink", "SINK_FN",
     "PRNG_OPT_MODE", "PRNG_OPT_BATCH_ITERS", "PRNG_OPT_RING_SLOTS", "PRNG_OPT_PROFILE",
-    "PRNG_OPT_KERNEL", "PRNG_OPT_GRID_WARPS", "PRNG_MODE_SERIAL", "PRNG_MODE_PAGEABLE",
+    "PRNG_OPT_KERNEL", "PRNG_OPT_GRID_WARPS", "PRNG_OPT_RING_PAD", "PRNG_MODE_SERIAL", "PRNG_MODE_PAGEABLE",
     "PRNG_MODE_OVERLAP1", "PRNG_MODE_OVERLAP2", "EV_NAMES",
 ]
 
 # ---------------------------------------------------------------- constants (include/prng.h)
 PRNG_OK, PRNG_EINVAL, PRNG_ESTATE, PRNG_ENOMEM, PRNG_ECUDA, PRNG_ESINK = 0, -1, -2, -3, -4, -5
 PRNG_OPT_MODE, PRNG_OPT_BATCH_ITERS, PRNG_OPT_RING_SLOTS = 1, 2, 3
-PRNG_OPT_PROFILE, PRNG_OPT_KERNEL, PRNG_OPT_GRID_WARPS = 4, 5, 6
+PRNG_OPT_PROFILE, PRNG_OPT_KERNEL, PRNG_OPT_GRID_WARPS, PRNG_OPT_RING_PAD = 4, 5, 6, 7
 PRNG_MODE_SERIAL, PRNG_MODE_PAGEABLE, PRNG_MODE_OVERLAP1, PRNG_MODE_OVERLAP2 = 0, 1, 2, 3
 EV_NAMES = ("INIT_KERNEL", "RNG_KERNEL", "READ_BUFFER", "OUT")
 
@@ -90,6 +90,7 @@ def lib():
         "prng_read_state": ([vp, vp, E], i32),
         "prng_set_option": ([vp, i32, i64, E], i32),
         "prng_get_option": ([vp, i32, ctypes.POINTER(i64), E], i32),
+        "prng_autotune": ([vp, u64, PD, E], i32),
         "prng_kernel_variants": ([], i32),
         "prng_kernel_variant_name": ([i32], ctypes.c_char_p),
         "prng_event_name": ([u32], ctypes.c_char_p),
@@ -224,6 +225,15 @@ def prng_get_option(h, option: int) -> int:
     v = i64()
     _check(lib().prng_get_option(h, option, ctypes.byref(v), ctypes.byref(err)), err)
     return v.value
+
+
+def prng_autotune(h, probe_iters: int = 0) -> float:
+    """Pick the fastest (kernel variant, warps per SM) for this handle's shape; returns the
+    winner's probe GB/s.  The handle must be prng_init'ed again afterwards."""
+    err = prng_err_t()
+    best = dbl()
+    _check(lib().prng_autotune(h, probe_iters, ctypes.byref(best), ctypes.byref(err)), err)
+    return best.value
 
 
 def prng_kernel_variants() -> int:

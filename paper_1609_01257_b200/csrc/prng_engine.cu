@@ -62,18 +62,26 @@ int ok(prng_err_t *err) {
 using BatchFn = void (*)(prngk::BatchArgs);
 struct Variant {
     const char *name;
-    int vec, npt, policy;
+    int vec, npt, policy, sync, cluster;  // sync: 0 none, 1 CTA barrier, 2 cluster barrier
+    int warps_per_sm;                     // default grid: resident warps per SM (0 = occupancy max)
     BatchFn fn;
 };
+#define V(name, vec, npt, pol, sync, cl, wps) \
+    {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>}
+// Measured on B200 at numrn = 2^24 x 1000, ring 16 x 128 MiB (profiles/r1_sweeps.md):
+// 8 CTA-synchronised warps per SM writing 16-B vectors reach ~7.9 TB/s; free-running
+// warps at full occupancy ~6.4 TB/s (too many drifting write streams).
 const Variant kVariants[] = {
-    {"v4n8", 4, 8, 0, prngk::batch_kernel<4, 8, 0>},     // default: 32-B stores, 8 numbers/thread
-    {"v2n4", 2, 4, 0, prngk::batch_kernel<2, 4, 0>},
-    {"v2n8", 2, 8, 0, prngk::batch_kernel<2, 8, 0>},
-    {"v4n4", 4, 4, 0, prngk::batch_kernel<4, 4, 0>},
-    {"v4n16", 4, 16, 0, prngk::batch_kernel<4, 16, 0>},
-    {"v4n8cs", 4, 8, 1, prngk::batch_kernel<4, 8, 1>},
-    {"v2n8cs", 2, 8, 1, prngk::batch_kernel<2, 8, 1>},
+    V("v2n4s1", 2, 4, 0, 1, 1, 8),  // default: 16-B stores, 4 numbers/thread, CTA barrier, 8 warps/SM
+    V("v2n8s1", 2, 8, 0, 1, 1, 4),    V("v2n16s1", 2, 16, 0, 1, 1, 4), V("v4n8s1", 4, 8, 0, 1, 1, 4),
+    // free-running warps
+    V("v4n8", 4, 8, 0, 0, 1, 0),      V("v2n4", 2, 4, 0, 0, 1, 0),     V("v2n8", 2, 8, 0, 0, 1, 0),
+    V("v4n4", 4, 4, 0, 0, 1, 0),      V("v4n16", 4, 16, 0, 0, 1, 0),   V("v2n16", 2, 16, 0, 0, 1, 0),
+    V("v4n8cs", 4, 8, 1, 0, 1, 0),    V("v2n8cs", 2, 8, 1, 0, 1, 0),
+    // cluster barrier (split arrive / wait) every iteration (c2 ~ s1; c4 ~ 4.4 TB/s)
+    V("v2n8c2", 2, 8, 0, 2, 2, 4),    V("v2n8c4", 2, 8, 0, 2, 4, 4),
 };
+#undef V
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kBlock = 256;
 
@@ -111,7 +119,7 @@ struct prng {
 
     // options
     int mode = PRNG_MODE_OVERLAP2;
-    int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0;
+    int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0, ring_pad = 0;
     int profile = 0, kernel = 0;
     int blocks_per_sm[kNumVariants] = {0};
 
@@ -206,14 +214,52 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     a.npieces = (h->count + piece - 1) / piece;
     // Persistent grid: at most one wave of resident warps; equalise pieces per warp.
     uint64_t max_warps = (uint64_t)h->blocks_per_sm[h->kernel] * h->num_sms * (kBlock / 32);
-    if (h->grid_warps > 0) max_warps = std::min<uint64_t>(max_warps, (uint64_t)h->grid_warps);
+    if (h->grid_warps > 0)
+        max_warps = std::min<uint64_t>(max_warps, (uint64_t)h->grid_warps);
+    else if (v.warps_per_sm > 0)
+        max_warps = std::min<uint64_t>(max_warps, (uint64_t)v.warps_per_sm * h->num_sms);
     max_warps = std::max<uint64_t>(max_warps, kBlock / 32);
     const uint64_t rounds0 = (a.npieces + max_warps - 1) / max_warps;
-    const uint64_t warps = (a.npieces + rounds0 - 1) / rounds0;
-    const uint64_t blocks = (warps + kBlock / 32 - 1) / (kBlock / 32);
-    a.rounds = (uint32_t)((a.npieces + blocks * (kBlock / 32) - 1) / (blocks * (kBlock / 32)));
+    uint64_t warps = (a.npieces + rounds0 - 1) / rounds0;
+    // Spread the warps over all SMs: with <= 8 warps per SM use one CTA per SM of
+    // ceil(warps / SMs) warps, else 256-thread CTAs.
+    uint64_t wpb = kBlock / 32;
+    if (warps <= (uint64_t)h->num_sms * wpb) wpb = std::max<uint64_t>(1, (warps + h->num_sms - 1) / h->num_sms);
+    uint64_t blocks = (warps + wpb - 1) / wpb;
+    const uint64_t C = (uint64_t)v.cluster;
+    if (C > 1) {
+        // whole clusters only, and no more clusters than can be co-resident
+        int max_cl = 0;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)C;
+        at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)(((blocks + C - 1) / C) * C));
+        cfg.blockDim = dim3((unsigned)(32 * wpb));
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CU(cudaOccupancyMaxActiveClusters(&max_cl, v.fn, &cfg));
+        if (max_cl < 1) return set_err(err, PRNG_ECUDA, "cluster of %llu CTAs cannot be resident", (unsigned long long)C);
+        blocks = std::min<uint64_t>((blocks + C - 1) / C, (uint64_t)max_cl) * C;
+    }
+    a.rounds = (uint32_t)((a.npieces + blocks * wpb - 1) / (blocks * wpb));
     if (int rc = prof_begin(h, s, PRNG_EV_RNG_KERNEL, err)) return rc;
-    v.fn<<<(unsigned)blocks, kBlock, 0, s>>>(a);
+    if (C > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)C;
+        at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)blocks);
+        cfg.blockDim = dim3((unsigned)(32 * wpb));
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CU(cudaLaunchKernelEx(&cfg, v.fn, a));
+    } else {
+        v.fn<<<(unsigned)blocks, (unsigned)(32 * wpb), 0, s>>>(a);
+    }
     CU(cudaGetLastError());
     return prof_end(h, s, err);
 }
@@ -387,6 +433,11 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             if (value < 0) return set_err(err, PRNG_EINVAL, "bad grid warps");
             h->grid_warps = value;
             break;
+        case PRNG_OPT_RING_PAD:
+            if (value < 0 || (value & 3) || value > (1 << 24)) return set_err(err, PRNG_EINVAL, "bad ring pad");
+            h->ring_pad = value;
+            break;
+
         default:
             return set_err(err, PRNG_EINVAL, "unknown option %d", option);
     }
@@ -402,6 +453,8 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_PROFILE: *value = h->profile; break;
         case PRNG_OPT_KERNEL: *value = h->kernel; break;
         case PRNG_OPT_GRID_WARPS: *value = h->grid_warps; break;
+        case PRNG_OPT_RING_PAD: *value = h->ring_pad; break;
+
         default: return set_err(err, PRNG_EINVAL, "unknown option %d", option);
     }
     return ok(err);
@@ -454,7 +507,7 @@ int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t ds
 }
 
 static int ensure_ring(prng *h, uint64_t numiter, prng_err_t *err) {
-    const uint64_t pitch = pitch_for(h->count);
+    const uint64_t pitch = pitch_for(h->count) + (uint64_t)h->ring_pad;
     uint64_t slots = (uint64_t)h->ring_slots_opt;
     if (slots == 0) {
         // >= 16 x L2 bytes (>= 2 GiB on B200) so write-back cannot be absorbed by L2.
@@ -490,6 +543,74 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
     CU(cudaStreamSynchronize(h->s_gen));
     h->wall_s += now_s() - t0;
     return PRNG_OK;
+}
+
+// ---------------------------------------------------------------------------- autotune
+// Which (variant, warps per SM) writes fastest depends on the shape (count, ring pitch,
+// slots) through the DRAM page / channel mapping, so measure instead of
+// guessing: each candidate generates `probe_iters` iterations into the handle's own ring
+// (best of 2 after a warm-up), the fastest becomes the handle's kernel + grid.  The
+// state array is consumed, so the handle needs prng_init afterwards.
+static const struct {
+    const char *variant;
+    int warps_per_sm;
+} kTuneCandidates[] = {{"v2n4s1", 8}, {"v2n8s1", 4}, {"v2n8s1", 8}, {"v2n16s1", 4},
+                       {"v2n16s1", 8}, {"v2n4s1", 4}, {"v4n8s1", 4}, {"v4n8s1", 8}};
+
+extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err) {
+    if (int rc = check_handle(h, err, false)) return rc;
+    if (int rc = ensure_ring(h, 0, err)) return rc;
+    if (probe_iters == 0)  // ~16 GiB of output per probe, within [8, 1000] iterations
+        probe_iters = std::min<uint64_t>(1000, std::max<uint64_t>(8, (16ull << 30) / (h->count * 8)));
+    const int saved_profile = h->profile;
+    h->profile = 0;
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    double best = -1;
+    int best_k = h->kernel;
+    int64_t best_w = h->grid_warps;
+    int rc = PRNG_OK;
+    for (const auto &c : kTuneCandidates) {
+        int k = -1;
+        for (int i = 0; i < kNumVariants; ++i)
+            if (!std::strcmp(kVariants[i].name, c.variant)) k = i;
+        if (k < 0) continue;
+        h->kernel = k;
+        h->grid_warps = (int64_t)c.warps_per_sm * h->num_sms;
+        double cand = 0;
+        for (int rep = 0; rep < 3 && !rc; ++rep) {
+            cudaEventRecord(e0, h->s_gen);
+            rc = launch_batch(h, h->d_ring, h->ring_pitch, h->ring_slots, 0, (uint32_t)probe_iters, false, h->s_gen,
+                              err);
+            cudaEventRecord(e1, h->s_gen);
+            if (rc) break;
+            cudaError_t e = cudaEventSynchronize(e1);
+            if (e != cudaSuccess) {
+                rc = set_err(err, PRNG_ECUDA, "autotune: %s", cudaGetErrorString(e));
+                break;
+            }
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0) cand = std::max(cand, 8.0 * h->count * probe_iters / (ms * 1e-3) / 1e9);
+        }
+        if (rc) break;
+        if (cand > best) {
+            best = cand;
+            best_k = k;
+            best_w = h->grid_warps;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h->profile = saved_profile;
+    h->kernel = best_k;
+    h->grid_warps = best_w;
+    h->inited = false;  // the probes consumed the state: prng_init before generating
+    h->pos = 0;
+    if (rc) return rc;
+    if (best_gbs) *best_gbs = best;
+    return ok(err);
 }
 
 // ---------------------------------------------------------------------------- end to end

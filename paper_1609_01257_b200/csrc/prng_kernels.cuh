@@ -140,15 +140,32 @@ struct BatchArgs {
     uint32_t rounds;          // ceil(npieces / warps in grid)
 };
 
-template <int VEC, int NPT, int POLICY, bool FULL>
-__device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base) {
+// Warp coherence (SYNC):
+//   0  none: every warp runs its piece at its own pace.
+//   1  CTA:  the warps of a CTA (adjacent pieces) meet at a named barrier every iteration,
+//            so a CTA writes one contiguous chunk per iteration.
+//   2  cluster: the CTAs of a thread-block cluster (adjacent pieces again) meet at a
+//            split hardware cluster barrier every iteration: arrive right after the
+//            iteration's stores are issued, wait just before the next iteration's stores,
+//            so the xorshift arithmetic overlaps the barrier.  Warps without a piece in
+//            the last round still take part in the barriers (IDLE mode).
+// Fewer drifting write streams -> fewer concurrently open DRAM pages.
+enum PieceMode { FULL = 0, PARTIAL = 1, IDLE = 2 };
+
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
+template <int VEC, int NPT, int POLICY, int SYNC, int MODE>
+__device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uint32_t bar_threads) {
     constexpr int NV = NPT / VEC;
     uint64_t x[NPT];
     // ---- load the NPT states of this lane (read once per launch)
-    if constexpr (FULL) {
+    if constexpr (MODE == FULL) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
-    } else {
+    } else if constexpr (MODE == PARTIAL) {
 #pragma unroll
         for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -156,25 +173,35 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base) {
                 const uint64_t idx = base + (uint64_t)v * 32 * VEC + e;
                 x[v * VEC + e] = idx < a.count ? a.state[idx] : 0ull;
             }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) x[j] = 0;
     }
     uint64_t *p = a.dst + (uint64_t)a.slot0 * a.pitch + base;
     const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
     uint32_t slot = a.slot0;
     for (uint32_t t = 0; t < a.iters; ++t) {
-        if (t > 0 || !a.first_is_state) {
+        if constexpr (MODE != IDLE) {
+            if (t > 0 || !a.first_is_state) {
 #pragma unroll
-            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
+                for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
+            }
         }
-        if constexpr (FULL) {
+        if constexpr (SYNC == 2) {
+            if (t > 0) cluster_wait();
+        }
+        if constexpr (MODE == FULL) {
 #pragma unroll
             for (int v = 0; v < NV; ++v) store_vec<VEC, POLICY>(p + v * 32 * VEC, x + v * VEC);
-        } else {
+        } else if constexpr (MODE == PARTIAL) {
 #pragma unroll
             for (int v = 0; v < NV; ++v)
 #pragma unroll
                 for (int e = 0; e < VEC; ++e)
                     if (base + (uint64_t)v * 32 * VEC + e < a.count) p[v * 32 * VEC + e] = x[v * VEC + e];
         }
+        if constexpr (SYNC == 1) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+        if constexpr (SYNC == 2) cluster_arrive();
         // advance to the next slot of the ring (warp-uniform)
         if (++slot == a.nslots) {
             slot = 0;
@@ -183,11 +210,12 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base) {
             p += a.pitch;
         }
     }
+    if constexpr (SYNC == 2) cluster_wait();  // balance the last arrive
     // ---- write the state back (== the launch's last iteration)
-    if constexpr (FULL) {
+    if constexpr (MODE == FULL) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
-    } else {
+    } else if constexpr (MODE == PARTIAL) {
 #pragma unroll
         for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -198,21 +226,33 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base) {
     }
 }
 
-template <int VEC, int NPT, int POLICY>
+template <int VEC, int NPT, int POLICY, int SYNC>
 __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
     constexpr uint64_t PIECE = 32ull * NPT;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t cta_warp0 = (uint64_t)blockIdx.x * wpb;
     for (uint32_t r = 0; r < a.rounds; ++r) {
         const uint64_t piece = (uint64_t)r * nwarps + warp;
-        if (piece >= a.npieces) break;  // warp-uniform
         const uint64_t base = piece * PIECE + (uint64_t)lane * VEC;
+        if (piece >= a.npieces) {  // warp-uniform
+            if constexpr (SYNC == 2) {
+                run_piece<VEC, NPT, POLICY, SYNC, IDLE>(a, base, 0);
+                continue;
+            } else {
+                break;
+            }
+        }
+        // warps of this CTA holding a piece in round r: a prefix of the CTA's warps
+        const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
+        const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - first < wpb ? a.npieces - first : wpb);
         if ((piece + 1) * PIECE <= a.count)
-            run_piece<VEC, NPT, POLICY, true>(a, base);
+            run_piece<VEC, NPT, POLICY, SYNC, FULL>(a, base, bar_threads);
         else
-            run_piece<VEC, NPT, POLICY, false>(a, base);
+            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL>(a, base, bar_threads);
     }
 }
 

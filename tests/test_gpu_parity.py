@@ -148,6 +148,49 @@ def test_device_only_ring_wraps():
         P.prng_destroy(h)
 
 
+def test_autotune_then_parity():
+    """prng_autotune picks a variant/grid, leaves the handle needing init, and the tuned
+    kernel is still bit-exact."""
+    n, i = 300007, 6
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        gbs = P.prng_autotune(h, 4)
+        assert gbs > 0
+        k = P.prng_get_option(h, P.PRNG_OPT_KERNEL)
+        assert 0 <= k < P.prng_kernel_variants() and P.prng_get_option(h, P.PRNG_OPT_GRID_WARPS) > 0
+        with pytest.raises(P.PrngError) as e:
+            P.prng_generate(h, 1)
+        assert e.value.code == P.PRNG_ESTATE
+        out = np.zeros((i, n), np.uint64)
+        P.prng_init(h)
+        P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0))
+    finally:
+        P.prng_destroy(h)
+    assert np.array_equal(out, oracle.stream(n, i, SEED_PARITY))
+
+
+@pytest.mark.parametrize("kv", range(14))
+def test_every_variant_device_only_wrapping_ring(kv):
+    """Each kernel variant through the device-only ring path (grid-strided rounds, ring
+    wrap-around inside one launch), vs the oracle at the ring slots and the state."""
+    if kv >= P.prng_kernel_variants():
+        pytest.skip("no such variant")
+    n, i = 200003, 11
+    h = P.prng_create(n, 9)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, kv)
+        P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, 4)
+        P.prng_set_option(h, P.PRNG_OPT_GRID_WARPS, 296)
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        want = oracle.stream(n, i, 9)
+        for k in range(i - 4, i):
+            assert np.array_equal(P.prng_read_slot(h, k % 4, n), want[k]), (P.prng_kernel_variant_name(kv), k)
+        assert np.array_equal(P.prng_read_state(h, n), want[-1])
+    finally:
+        P.prng_destroy(h)
+
+
 @pytest.mark.slow
 def test_full_size_config2_sampled():
     """BASELINE config 2 in bench.py's launch configuration (n = 2^24, numiter = 1000,

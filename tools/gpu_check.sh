@@ -6,14 +6,16 @@ TAG=${1:-r1}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
-nvidia-smi topo -m > $OUT/topo.txt 2>&1
-lscpu > $OUT/lscpu.txt 2>&1; nproc >> $OUT/lscpu.txt; free -g >> $OUT/lscpu.txt
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
+timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+# ncu: the default variant (id 0) in bench.py's launch configuration, no autotune probes
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-probes > $OUT/ncu_launches.log 2>&1
+    python bench.py --kernel 0 --steps 2 --warmup 1 --no-e2e --no-cpu --no-probes > $OUT/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:batch_kernel -s 1 -c 1 \
-    -o $OUT/prof_batch python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-probes > $OUT/ncu_full.log 2>&1
+    -o $OUT/prof_batch python bench.py --kernel 0 --steps 1 --warmup 1 --no-e2e --no-cpu --no-probes > $OUT/ncu_full.log 2>&1
+timeout 600 ncu --metrics dram__bytes_write.sum,dram__bytes_read.sum,gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/dram_lin.csv python bench.py --kernel 0 --numiter 250 --steps 1 --warmup 1 --no-e2e --no-cpu --no-probes > /dev/null 2>&1
 ls -la $OUT
