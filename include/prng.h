@@ -98,7 +98,9 @@ int prng_init(prng_t *h, prng_err_t *err);
  *    copied D2H on a side stream into a pinned host double buffer and handed to `sink`
  *    while the next batches are generated and copied (P:164-173, P:177 limitation 2).
  *  sink == NULL (device only): iterations are generated into the handle's device ring of
- *    R slots (slot = iteration mod R) with no host transfer; see prng_device_ring().
+ *    R slots with no host transfer; see prng_device_ring().  The ring is large (64 GiB,
+ *    capped at 40 % of free HBM) and rotating, so no address is rewritten within 64 GiB of
+ *    output -- see DESIGN.md §5 for why that matters on B200.
  * Repeated calls continue the stream: generate(a); generate(b) == generate(a + b) (A10).
  * Blocks until all work of the call is complete. */
 int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, prng_err_t *err);
@@ -112,10 +114,12 @@ int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t ds
                          uint64_t dst_slots, void *stream, prng_err_t *err);
 
 /* The handle's device ring (device-only mode): base pointer, pitch (u64 elements), number
- * of slots, and the iteration held by slot 0 .. slots-1 is `iteration mod slots`.
- * `last_iter_end` = stream position (iterations emitted so far). */
+ * of slots R, and the slot holding iteration 0 of the current prng_init: iteration k
+ * (k < last_iter_end, the stream position) was written to slot (iter0_slot + k) mod R and
+ * is still there if k >= last_iter_end - R.  The write cursor rotates across prng_init
+ * calls (iter0_slot changes). */
 int prng_device_ring(const prng_t *h, uint64_t **base, uint64_t *pitch, uint64_t *slots,
-                     uint64_t *last_iter_end, prng_err_t *err);
+                     uint64_t *iter0_slot, uint64_t *last_iter_end, prng_err_t *err);
 
 /* Copy `count` outputs of device-ring slot `slot` to host memory (test/inspection aid). */
 int prng_read_slot(prng_t *h, uint64_t slot, uint64_t *host_dst, prng_err_t *err);
@@ -127,12 +131,14 @@ int prng_read_state(prng_t *h, uint64_t *host_dst, prng_err_t *err);
 enum prng_option {
     PRNG_OPT_MODE = 1,         /* enum prng_mode, default PRNG_MODE_OVERLAP2            */
     PRNG_OPT_BATCH_ITERS = 2,  /* T for end-to-end batches; 0 = auto (~256 MiB per batch) */
-    PRNG_OPT_RING_SLOTS = 3,   /* R of the device-only ring; 0 = auto (>= 16x L2 bytes)   */
+    PRNG_OPT_RING_SLOTS = 3,   /* R of the device-only ring; 0 = auto (64 GiB, <= 40 % free) */
     PRNG_OPT_PROFILE = 4,      /* 1 = record per-batch intervals (CUDA events)           */
     PRNG_OPT_KERNEL = 5,       /* kernel variant id (see prng_kernel_variants); 0 = default */
     PRNG_OPT_GRID_WARPS = 6,   /* cap on resident warps of the persistent grid; 0 = auto  */
-    PRNG_OPT_RING_PAD = 7      /* extra u64 elements between device-only ring slots (multiple
+    PRNG_OPT_RING_PAD = 7,     /* extra u64 elements between device-only ring slots (multiple
                                   of 4; breaks power-of-two slot strides); default 0       */
+    PRNG_OPT_HOST_MEM = 8      /* pinned host halves of modes O1/O2/S0: 0 cudaHostAlloc,
+                                  1 write-combined, 2 THP-backed mmap + cudaHostRegister  */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two
@@ -142,7 +148,10 @@ enum prng_mode {
     PRNG_MODE_PAGEABLE = 1,  /* S1: side stream, but pageable (malloc) host buffers             */
     PRNG_MODE_OVERLAP1 = 2,  /* O1: side copy stream + device double buffer, ONE pinned host
                                 buffer: read and out serialised as in the paper */
-    PRNG_MODE_OVERLAP2 = 3   /* O2: O1 + host-side dual buffer, sink(j) || D2H(j+1) || gen(j+2) */
+    PRNG_MODE_OVERLAP2 = 3,  /* O2: O1 + host-side dual buffer, sink(j) || D2H(j+1) || gen(j+2) */
+    PRNG_MODE_ZEROCOPY = 4   /* O3: the kernel stores each batch straight into mapped pinned host
+                                memory (two halves): generation and transfer fused, no device ring
+                                and no copy engine; sink(j) || gen(j+1).  Needs count % 4 == 0. */
 };
 
 int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err);

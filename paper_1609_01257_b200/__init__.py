@@ -23,15 +23,15 @@ __all__ = [
     "prng_probe_store_gbs", "prng_probe_d2h_gbs", "SINK_NULL", "SINK_COPY", "SINK_DIGEST",
     "CopySink", "DigestSink", "SINK_FN",
     "PRNG_OPT_MODE", "PRNG_OPT_BATCH_ITERS", "PRNG_OPT_RING_SLOTS", "PRNG_OPT_PROFILE",
-    "PRNG_OPT_KERNEL", "PRNG_OPT_GRID_WARPS", "PRNG_OPT_RING_PAD", "PRNG_MODE_SERIAL", "PRNG_MODE_PAGEABLE",
+    "PRNG_OPT_KERNEL", "PRNG_OPT_GRID_WARPS", "PRNG_OPT_RING_PAD", "PRNG_OPT_HOST_MEM", "PRNG_MODE_ZEROCOPY", "PRNG_MODE_SERIAL", "PRNG_MODE_PAGEABLE",
     "PRNG_MODE_OVERLAP1", "PRNG_MODE_OVERLAP2", "EV_NAMES",
 ]
 
 # ---------------------------------------------------------------- constants (include/prng.h)
 PRNG_OK, PRNG_EINVAL, PRNG_ESTATE, PRNG_ENOMEM, PRNG_ECUDA, PRNG_ESINK = 0, -1, -2, -3, -4, -5
 PRNG_OPT_MODE, PRNG_OPT_BATCH_ITERS, PRNG_OPT_RING_SLOTS = 1, 2, 3
-PRNG_OPT_PROFILE, PRNG_OPT_KERNEL, PRNG_OPT_GRID_WARPS, PRNG_OPT_RING_PAD = 4, 5, 6, 7
-PRNG_MODE_SERIAL, PRNG_MODE_PAGEABLE, PRNG_MODE_OVERLAP1, PRNG_MODE_OVERLAP2 = 0, 1, 2, 3
+PRNG_OPT_PROFILE, PRNG_OPT_KERNEL, PRNG_OPT_GRID_WARPS, PRNG_OPT_RING_PAD, PRNG_OPT_HOST_MEM = 4, 5, 6, 7, 8
+PRNG_MODE_SERIAL, PRNG_MODE_PAGEABLE, PRNG_MODE_OVERLAP1, PRNG_MODE_OVERLAP2, PRNG_MODE_ZEROCOPY = 0, 1, 2, 3, 4
 EV_NAMES = ("INIT_KERNEL", "RNG_KERNEL", "READ_BUFFER", "OUT")
 
 u64, u32, i32, i64, dbl = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64, ctypes.c_double
@@ -85,7 +85,7 @@ def lib():
         "prng_init": ([vp, E], i32),
         "prng_generate": ([vp, u64, vp, vp, E], i32),
         "prng_generate_device": ([vp, u64, vp, u64, u64, vp, E], i32),
-        "prng_device_ring": ([vp, ctypes.POINTER(vp), P64, P64, P64, E], i32),
+        "prng_device_ring": ([vp, ctypes.POINTER(vp), P64, P64, P64, P64, E], i32),
         "prng_read_slot": ([vp, u64, vp, E], i32),
         "prng_read_state": ([vp, vp, E], i32),
         "prng_set_option": ([vp, i32, i64, E], i32),
@@ -194,11 +194,13 @@ def prng_generate_device(h, numiter: int, dst_ptr: int, dst_pitch: int, dst_slot
 
 
 def prng_device_ring(h):
+    """-> (base, pitch, slots, iter0_slot, last_iter_end); iteration k sits in slot
+    (iter0_slot + k) % slots."""
     err = prng_err_t()
-    base, pitch, slots, end = vp(), u64(), u64(), u64()
+    base, pitch, slots, first, end = vp(), u64(), u64(), u64(), u64()
     _check(lib().prng_device_ring(h, ctypes.byref(base), ctypes.byref(pitch), ctypes.byref(slots),
-                                  ctypes.byref(end), ctypes.byref(err)), err)
-    return base.value, pitch.value, slots.value, end.value
+                                  ctypes.byref(first), ctypes.byref(end), ctypes.byref(err)), err)
+    return base.value, pitch.value, slots.value, first.value, end.value
 
 
 def prng_read_slot(h, slot: int, count: int) -> np.ndarray:

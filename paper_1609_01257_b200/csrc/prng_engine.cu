@@ -11,6 +11,7 @@
 //   limitation 2 (host-side dual buffer) -> two pinned host halves (mode O2)
 //   limitation 3 (no vectorisation) -> NPT numbers per thread, 32-byte stores
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <chrono>
@@ -68,11 +69,12 @@ struct Variant {
 };
 #define V(name, vec, npt, pol, sync, cl, wps) \
     {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>}
-// Measured on B200 at numrn = 2^24 x 1000, ring 16 x 128 MiB (profiles/r1_sweeps.md):
-// 8 CTA-synchronised warps per SM writing 16-B vectors reach ~7.9 TB/s; free-running
-// warps at full occupancy ~6.4 TB/s (too many drifting write streams).
+// Measured on B200 at numrn = 2^24 x 1000 through a non-reused 64 GiB ring
+// (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 16-B vectors reach
+// ~6.9 TB/s (93 % of the same-box cudaMemset fill rate); free-running warps at full
+// occupancy ~6.2 TB/s (more concurrently open DRAM pages).
 const Variant kVariants[] = {
-    V("v2n4s1", 2, 4, 0, 1, 1, 8),  // default: 16-B stores, 4 numbers/thread, CTA barrier, 8 warps/SM
+    V("v2n4s1", 2, 4, 0, 1, 1, 4),  // default: 16-B stores, 4 numbers/thread, CTA barrier, 4 warps/SM
     V("v2n8s1", 2, 8, 0, 1, 1, 4),    V("v2n16s1", 2, 16, 0, 1, 1, 4), V("v4n8s1", 4, 8, 0, 1, 1, 4),
     // free-running warps
     V("v4n8", 4, 8, 0, 0, 1, 0),      V("v2n4", 2, 4, 0, 0, 1, 0),     V("v2n8", 2, 8, 0, 0, 1, 0),
@@ -105,12 +107,16 @@ struct prng {
     // device-only ring
     uint64_t *d_ring = nullptr;
     uint64_t ring_pitch = 0, ring_slots = 0;
+    uint64_t ring_cursor = 0;  // next slot to write; persists across prng_init (rotating ring)
+    uint64_t ring_iter0 = 0;   // slot holding iteration 0 of the current init
 
     // end-to-end buffers
     uint64_t *d_buf = nullptr;  // 2 halves x T slots, pitch buf_pitch
     uint64_t buf_pitch = 0, buf_T = 0;
     uint64_t *h_buf[2] = {nullptr, nullptr};
-    bool h_pinned = false;
+    uint64_t *h_dev[2] = {nullptr, nullptr};  // device aliases of mapped host halves (zero-copy)
+    int h_kind = -1;                          // enum HostKind of the allocated halves
+    int host_mem = 0;                         // PRNG_OPT_HOST_MEM
     uint64_t h_T = 0;
     int h_halves = 0;
 
@@ -141,6 +147,23 @@ struct prng {
 
 namespace {
 
+// Host buffer kinds (PRNG_OPT_HOST_MEM selects among the pinned ones).
+enum HostKind { HK_PINNED = 0, HK_PINNED_WC = 1, HK_HUGE_REGISTERED = 2, HK_MAPPED = 3, HK_PAGEABLE = 4 };
+
+void free_host(int kind, void *p, size_t bytes) {
+    if (!p) return;
+    switch (kind) {
+        case HK_PINNED:
+        case HK_PINNED_WC:
+        case HK_MAPPED: cudaFreeHost(p); break;
+        case HK_HUGE_REGISTERED:
+            cudaHostUnregister(p);
+            munmap(p, bytes);
+            break;
+        default: std::free(p);
+    }
+}
+
 uint64_t pitch_for(uint64_t count) { return (count + 3) & ~3ull; }  // 32-byte aligned slots
 
 void free_e2e(prng *h) {
@@ -148,13 +171,8 @@ void free_e2e(prng *h) {
     h->d_buf = nullptr;
     h->buf_T = 0;
     for (int i = 0; i < 2; ++i) {
-        if (h->h_buf[i]) {
-            if (h->h_pinned)
-                cudaFreeHost(h->h_buf[i]);
-            else
-                std::free(h->h_buf[i]);
-        }
-        h->h_buf[i] = nullptr;
+        free_host(h->h_kind, h->h_buf[i], h->h_T * h->count * sizeof(uint64_t));
+        h->h_buf[i] = h->h_dev[i] = nullptr;
     }
     h->h_T = 0;
     h->h_halves = 0;
@@ -402,7 +420,7 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
     if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
     switch (option) {
         case PRNG_OPT_MODE:
-            if (value < PRNG_MODE_SERIAL || value > PRNG_MODE_OVERLAP2) return set_err(err, PRNG_EINVAL, "bad mode");
+            if (value < PRNG_MODE_SERIAL || value > PRNG_MODE_ZEROCOPY) return set_err(err, PRNG_EINVAL, "bad mode");
             if (value != h->mode) free_e2e(h);
             h->mode = (int)value;
             break;
@@ -437,6 +455,10 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             if (value < 0 || (value & 3) || value > (1 << 24)) return set_err(err, PRNG_EINVAL, "bad ring pad");
             h->ring_pad = value;
             break;
+        case PRNG_OPT_HOST_MEM:
+            if (value < HK_PINNED || value > HK_HUGE_REGISTERED) return set_err(err, PRNG_EINVAL, "bad host mem kind");
+            h->host_mem = (int)value;
+            break;
 
         default:
             return set_err(err, PRNG_EINVAL, "unknown option %d", option);
@@ -454,6 +476,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_KERNEL: *value = h->kernel; break;
         case PRNG_OPT_GRID_WARPS: *value = h->grid_warps; break;
         case PRNG_OPT_RING_PAD: *value = h->ring_pad; break;
+        case PRNG_OPT_HOST_MEM: *value = h->host_mem; break;
 
         default: return set_err(err, PRNG_EINVAL, "unknown option %d", option);
     }
@@ -477,6 +500,7 @@ int prng_init(prng_t *h, prng_err_t *err) {
     CU(cudaGetLastError());
     if (int rc = prof_end(h, h->s_gen, err)) return rc;
     h->pos = 0;
+    h->ring_iter0 = h->ring_cursor;
     h->inited = true;
     if (h->profile) {
         CU(cudaStreamSynchronize(h->s_gen));
@@ -506,13 +530,29 @@ int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t ds
     return ok(err);
 }
 
+// Device-only ring.  B200 measurement (profiles/r1_ring_absorption.md): when the same
+// addresses are rewritten within a few GiB, ncu's dram__bytes_write drops far below the
+// bytes stored (2.3 GB DRAM writes for 134 GB stored through a 2 GiB ring; 11 GB through
+// 4 GiB; 84 GB through 8 GiB; 128 GB through 16 GiB; all 134 GB at >= 32 GiB) and the
+// kernel runs ~25 % faster -- a benchmark artefact, not sustainable output bandwidth.  So
+// the default ring is large (kRingBytes, capped at 40 % of free HBM) and ROTATES: the
+// write cursor persists across prng_init, so the reuse distance of any address is the
+// whole ring, also across repeated runs.
+constexpr uint64_t kRingBytes = 64ull << 30;
+
 static int ensure_ring(prng *h, uint64_t numiter, prng_err_t *err) {
     const uint64_t pitch = pitch_for(h->count) + (uint64_t)h->ring_pad;
+    const uint64_t slot_bytes = pitch * sizeof(uint64_t);
     uint64_t slots = (uint64_t)h->ring_slots_opt;
     if (slots == 0) {
-        // >= 16 x L2 bytes (>= 2 GiB on B200) so write-back cannot be absorbed by L2.
-        const uint64_t want = std::max<uint64_t>(16ull * (uint64_t)std::max(h->l2_bytes, 1 << 20), 2ull << 30);
-        slots = std::max<uint64_t>(2, (want + pitch * 8 - 1) / (pitch * 8));
+        uint64_t target = kRingBytes;
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            uint64_t have = (uint64_t)free_b + (h->d_ring ? h->ring_slots * h->ring_pitch * 8 : 0);
+            target = std::min<uint64_t>(target, have * 2 / 5);
+        }
+        slots = std::max<uint64_t>(2, target / slot_bytes);
+        slots = std::min<uint64_t>(slots, 0x7FFFFFFFull);
     }
     if (h->d_ring && h->ring_slots == slots && h->ring_pitch == pitch) return PRNG_OK;
     if (h->d_ring) {
@@ -520,9 +560,11 @@ static int ensure_ring(prng *h, uint64_t numiter, prng_err_t *err) {
         cudaFree(h->d_ring);
         h->d_ring = nullptr;
     }
-    CU(cudaMalloc(&h->d_ring, slots * pitch * sizeof(uint64_t)));
+    CU(cudaMalloc(&h->d_ring, slots * slot_bytes));
     h->ring_slots = slots;
     h->ring_pitch = pitch;
+    h->ring_cursor = 0;
+    h->ring_iter0 = (slots - (h->pos % slots)) % slots;  // keep "iteration k -> (iter0 + k) mod R"
     (void)numiter;
     return PRNG_OK;
 }
@@ -534,12 +576,13 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
     uint64_t done = 0;
     while (done < numiter) {
         const uint32_t it = (uint32_t)std::min<uint64_t>(numiter - done, 0x7FFFFFFFull);
-        if (int rc = launch_batch(h, h->d_ring, h->ring_pitch, h->ring_slots, h->pos % h->ring_slots, it,
+        if (int rc = launch_batch(h, h->d_ring, h->ring_pitch, h->ring_slots, (h->ring_iter0 + h->pos) % h->ring_slots, it,
                                   h->pos == 0, h->s_gen, err))
             return rc;
         h->pos += it;
         done += it;
     }
+    h->ring_cursor = (h->ring_iter0 + h->pos) % h->ring_slots;
     CU(cudaStreamSynchronize(h->s_gen));
     h->wall_s += now_s() - t0;
     return PRNG_OK;
@@ -554,8 +597,8 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
 static const struct {
     const char *variant;
     int warps_per_sm;
-} kTuneCandidates[] = {{"v2n4s1", 8}, {"v2n8s1", 4}, {"v2n8s1", 8}, {"v2n16s1", 4},
-                       {"v2n16s1", 8}, {"v2n4s1", 4}, {"v4n8s1", 4}, {"v4n8s1", 8}};
+} kTuneCandidates[] = {{"v2n4s1", 4}, {"v2n4s1", 8}, {"v2n8s1", 4}, {"v2n8s1", 8},
+                       {"v2n16s1", 4}, {"v2n8c2", 4}, {"v4n8s1", 4}, {"v2n8", 4}};
 
 extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err) {
     if (int rc = check_handle(h, err, false)) return rc;
@@ -581,9 +624,10 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
         double cand = 0;
         for (int rep = 0; rep < 3 && !rc; ++rep) {
             cudaEventRecord(e0, h->s_gen);
-            rc = launch_batch(h, h->d_ring, h->ring_pitch, h->ring_slots, 0, (uint32_t)probe_iters, false, h->s_gen,
+            rc = launch_batch(h, h->d_ring, h->ring_pitch, h->ring_slots, h->ring_cursor, (uint32_t)probe_iters, false, h->s_gen,
                               err);
             cudaEventRecord(e1, h->s_gen);
+            h->ring_cursor = (h->ring_cursor + probe_iters) % h->ring_slots;
             if (rc) break;
             cudaError_t e = cudaEventSynchronize(e1);
             if (e != cudaSuccess) {
@@ -614,33 +658,97 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
 }
 
 // ---------------------------------------------------------------------------- end to end
-static int ensure_e2e(prng *h, uint64_t T, int halves, bool pinned, prng_err_t *err) {
+static int ensure_e2e(prng *h, uint64_t T, int halves, int kind, bool need_dbuf, prng_err_t *err) {
     const uint64_t pitch = pitch_for(h->count);
-    if (!h->d_buf || h->buf_T != T || h->buf_pitch != pitch) {
+    if (need_dbuf && (!h->d_buf || h->buf_T != T || h->buf_pitch != pitch)) {
         if (h->d_buf) cudaFree(h->d_buf);
         h->d_buf = nullptr;
         CU(cudaMalloc(&h->d_buf, 2 * T * pitch * sizeof(uint64_t)));
         h->buf_T = T;
         h->buf_pitch = pitch;
     }
-    if (h->h_T != T || h->h_halves != halves || h->h_pinned != pinned) {
+    if (h->h_T != T || h->h_halves < halves || h->h_kind != kind) {
         for (int i = 0; i < 2; ++i) {
-            if (h->h_buf[i]) h->h_pinned ? (void)cudaFreeHost(h->h_buf[i]) : std::free(h->h_buf[i]);
-            h->h_buf[i] = nullptr;
+            free_host(h->h_kind, h->h_buf[i], h->h_T * h->count * sizeof(uint64_t));
+            h->h_buf[i] = h->h_dev[i] = nullptr;
         }
+        h->h_kind = kind;
+        h->h_T = T;
+        h->h_halves = 0;
         const size_t bytes = T * h->count * sizeof(uint64_t);
         for (int i = 0; i < halves; ++i) {
-            if (pinned) {
-                CU(cudaHostAlloc(&h->h_buf[i], bytes, cudaHostAllocDefault));
-            } else {
-                h->h_buf[i] = (uint64_t *)std::malloc(bytes);
-                if (!h->h_buf[i]) return set_err(err, PRNG_ENOMEM, "malloc(%zu)", bytes);
+            void *p = nullptr;
+            switch (kind) {
+                case HK_PINNED: CU(cudaHostAlloc(&p, bytes, cudaHostAllocDefault)); break;
+                case HK_PINNED_WC: CU(cudaHostAlloc(&p, bytes, cudaHostAllocWriteCombined)); break;
+                case HK_MAPPED: CU(cudaHostAlloc(&p, bytes, cudaHostAllocMapped)); break;
+                case HK_HUGE_REGISTERED: {
+                    // anonymous mapping advised onto 2 MiB transparent huge pages, then pinned
+                    p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+                    if (p == MAP_FAILED) return set_err(err, PRNG_ENOMEM, "mmap(%zu)", bytes);
+                    madvise(p, bytes, MADV_HUGEPAGE);
+                    std::memset(p, 0, bytes);
+                    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterDefault);
+                    if (e != cudaSuccess) {
+                        munmap(p, bytes);
+                        return set_err(err, PRNG_ECUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+                    }
+                    break;
+                }
+                default:
+                    p = std::malloc(bytes);
+                    if (!p) return set_err(err, PRNG_ENOMEM, "malloc(%zu)", bytes);
             }
+            h->h_buf[i] = (uint64_t *)p;
+            if (kind == HK_MAPPED) CU(cudaHostGetDevicePointer((void **)&h->h_dev[i], p, 0));
+            h->h_halves = i + 1;
         }
-        h->h_T = T;
-        h->h_halves = halves;
-        h->h_pinned = pinned;
     }
+    return PRNG_OK;
+}
+
+// O3 (zero-copy): the generation kernel stores each batch straight into a mapped pinned
+// host half over PCIe -- no device ring, no copy engine; the store IS the transfer.
+// sink(j) runs while gen(j+1) writes the other half; gen(j+2) is enqueued after sink(j).
+static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, prng_sink_fn sink, void *user,
+                             prng_err_t *err) {
+    if (h->count % 4) return set_err(err, PRNG_EINVAL, "zero-copy mode needs count %% 4 == 0 (32-B aligned rows)");
+    if (int rc = ensure_e2e(h, T, 2, HK_MAPPED, false, err)) return rc;
+    const uint64_t nb = (numiter + T - 1) / T;
+    const uint64_t pos0 = h->pos;
+    auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    for (auto &e : ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int rc = PRNG_OK;
+    auto gen = [&](uint64_t j) -> int {
+        if (int r = launch_batch(h, h->h_dev[j & 1], h->count, T, 0, iters_of(j), pos0 + j * T == 0, h->s_gen, err))
+            return r;
+        cudaError_t e = cudaEventRecord(ev[j & 1], h->s_gen);
+        return e == cudaSuccess ? PRNG_OK : set_err(err, PRNG_ECUDA, "cudaEventRecord: %s", cudaGetErrorString(e));
+    };
+    for (uint64_t j = 0; j < std::min<uint64_t>(nb, 2) && !rc; ++j) rc = gen(j);
+    for (uint64_t j = 0; j < nb && !rc; ++j) {
+        cudaError_t e = cudaEventSynchronize(ev[j & 1]);
+        if (e != cudaSuccess) {
+            rc = set_err(err, PRNG_ECUDA, "cudaEventSynchronize: %s", cudaGetErrorString(e));
+            break;
+        }
+        const double a = now_s();
+        int r = sink(user, pos0 + j * T, iters_of(j), h->gid_begin, h->count, h->h_buf[j & 1]);
+        if (h->profile) h->host_iv.push_back({PRNG_EV_OUT, a - h->host_origin, now_s() - h->host_origin});
+        if (r != 0) {
+            rc = set_err(err, PRNG_ESINK, "sink returned %d at batch %llu", r, (unsigned long long)j);
+            break;
+        }
+        if (j + 2 < nb) rc = gen(j + 2);
+    }
+    cudaStreamSynchronize(h->s_gen);
+    for (auto &e : ev) cudaEventDestroy(e);
+    if (rc) {
+        h->poisoned = true;
+        return rc;
+    }
+    h->pos = pos0 + numiter;
     return PRNG_OK;
 }
 
@@ -662,8 +770,15 @@ static int generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void *user
     if (T == 0) T = std::max<uint64_t>(1, (256ull << 20) / row);  // ~256 MiB per batch
     T = std::min<uint64_t>(T, numiter);
     const int mode = h->mode;
+    if (mode == PRNG_MODE_ZEROCOPY) {
+        const double tz = now_s();
+        int rc = generate_zerocopy(h, numiter, T, sink, user, err);
+        h->wall_s += now_s() - tz;
+        return rc;
+    }
     const int halves = (mode == PRNG_MODE_OVERLAP2 || mode == PRNG_MODE_PAGEABLE) ? 2 : 1;
-    if (int rc = ensure_e2e(h, T, halves, mode != PRNG_MODE_PAGEABLE, err)) return rc;
+    if (int rc = ensure_e2e(h, T, halves, mode == PRNG_MODE_PAGEABLE ? HK_PAGEABLE : h->host_mem, true, err))
+        return rc;
     const uint64_t nb = (numiter + T - 1) / T;
     const uint64_t pitch = h->buf_pitch;
     auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
@@ -786,9 +901,11 @@ int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, pr
     return ok(err);
 }
 
-int prng_device_ring(const prng_t *h, uint64_t **base, uint64_t *pitch, uint64_t *slots, uint64_t *last_iter_end,
-                     prng_err_t *err) {
-    if (!h || !base || !pitch || !slots || !last_iter_end) return set_err(err, PRNG_EINVAL, "NULL argument");
+int prng_device_ring(const prng_t *h, uint64_t **base, uint64_t *pitch, uint64_t *slots, uint64_t *iter0_slot,
+                     uint64_t *last_iter_end, prng_err_t *err) {
+    if (!h || !base || !pitch || !slots || !iter0_slot || !last_iter_end)
+        return set_err(err, PRNG_EINVAL, "NULL argument");
+    *iter0_slot = h->ring_iter0;
     *base = h->d_ring;
     *pitch = h->ring_pitch;
     *slots = h->ring_slots;

@@ -138,12 +138,19 @@ def test_device_only_ring_wraps():
         P.prng_init(h)
         P.prng_generate(h, 3)
         P.prng_generate(h, 5)
-        base, pitch, slots, end = P.prng_device_ring(h)
-        assert slots == 3 and end == 8
+        base, pitch, slots, first, end = P.prng_device_ring(h)
+        assert slots == 3 and end == 8 and first == 0
         want = oracle.stream(n, 8, 2)
         for k in range(5, 8):
-            assert np.array_equal(P.prng_read_slot(h, k % slots, n), want[k])
+            assert np.array_equal(P.prng_read_slot(h, (first + k) % slots, n), want[k])
         assert np.array_equal(P.prng_read_state(h, n), want[7])
+        # the cursor rotates across prng_init: a second run starts where the first stopped
+        P.prng_init(h)
+        P.prng_generate(h, 2)
+        _, _, _, first2, end2 = P.prng_device_ring(h)
+        assert first2 == 8 % 3 and end2 == 2
+        for k in range(2):
+            assert np.array_equal(P.prng_read_slot(h, (first2 + k) % slots, n), want[k])
     finally:
         P.prng_destroy(h)
 
@@ -184,8 +191,9 @@ def test_every_variant_device_only_wrapping_ring(kv):
         P.prng_init(h)
         P.prng_generate(h, i)
         want = oracle.stream(n, i, 9)
+        _, _, _, first, _ = P.prng_device_ring(h)
         for k in range(i - 4, i):
-            assert np.array_equal(P.prng_read_slot(h, k % 4, n), want[k]), (P.prng_kernel_variant_name(kv), k)
+            assert np.array_equal(P.prng_read_slot(h, (first + k) % 4, n), want[k]), (P.prng_kernel_variant_name(kv), k)
         assert np.array_equal(P.prng_read_state(h, n), want[-1])
     finally:
         P.prng_destroy(h)
@@ -201,17 +209,17 @@ def test_full_size_config2_sampled():
     try:
         P.prng_init(h)
         P.prng_generate(h, i)
-        _, pitch, slots, end = P.prng_device_ring(h)
+        _, pitch, slots, first, end = P.prng_device_ring(h)
         g, k = sample_points(n, i, 2000, rng_seed=99)
         st = P.prng_read_state(h, n)
         for gg in g[:500]:
             assert int(st[gg]) == oracle.sample(int(gg), i - 1, 0)
         for kk in sorted({i - 1, i - slots, i - slots // 2}):
-            row = P.prng_read_slot(h, kk % slots, n)
+            row = P.prng_read_slot(h, (first + kk) % slots, n)
             for gg in g[:300]:
                 assert int(row[gg]) == oracle.sample(int(gg), kk, 0)
         # one whole slot: every gid at the last iteration equals the state
-        assert np.array_equal(P.prng_read_slot(h, (i - 1) % slots, n), st)
+        assert np.array_equal(P.prng_read_slot(h, (first + i - 1) % slots, n), st)
     finally:
         P.prng_destroy(h)
 
@@ -288,3 +296,33 @@ def test_profile_causality(mode):
         if j + 2 < nb:
             assert rng[j + 2][0] >= rd[j][1] - eps
     assert wall > 0
+
+
+@pytest.mark.parametrize("batch", [0, 1, 3])
+def test_zerocopy_mode(batch):
+    """O3: the kernel writes straight into mapped pinned host memory."""
+    n, i = 6000, 13
+    assert np.array_equal(run_e2e(n, i, 21, mode=P.PRNG_MODE_ZEROCOPY, batch=batch), oracle.stream(n, i, 21))
+
+
+def test_zerocopy_needs_aligned_rows():
+    with pytest.raises(P.PrngError) as e:
+        run_e2e(1001, 3, mode=P.PRNG_MODE_ZEROCOPY)
+    assert e.value.code == P.PRNG_EINVAL
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_host_memory_kinds(kind):
+    """Write-combined and THP-registered pinned halves give the same stream."""
+    n, i = 4096 + 8, 9
+    count = n
+    h = P.prng_create(n, 3)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_HOST_MEM, kind)
+        P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 2)
+        out = np.zeros((i, count), np.uint64)
+        P.prng_init(h)
+        P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), count, 0, i, 0))
+    finally:
+        P.prng_destroy(h)
+    assert np.array_equal(out, oracle.stream(n, i, 3))

@@ -59,7 +59,7 @@ def main():
                 P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, slots)
                 P.prng_set_option(h, P.PRNG_OPT_RING_PAD, pad)
                 best, med = run(h, a.numrn, a.numiter, a.reps, gen)
-                _, _, rs, _ = P.prng_device_ring(h)
+                _, _, rs, _, _ = P.prng_device_ring(h)
                 P.prng_destroy(h)
                 print(json.dumps({"variant": P.prng_kernel_variant_name(v), "grid_warps": w, "slots": rs, "pad": pad,
                                   "best_gbs": round(best, 1), "median_gbs": round(med, 1)}), flush=True)
