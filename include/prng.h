@@ -137,8 +137,10 @@ enum prng_option {
     PRNG_OPT_GRID_WARPS = 6,   /* cap on resident warps of the persistent grid; 0 = auto  */
     PRNG_OPT_RING_PAD = 7,     /* extra u64 elements between device-only ring slots (multiple
                                   of 4; breaks power-of-two slot strides); default 0       */
-    PRNG_OPT_HOST_MEM = 8      /* pinned host halves of modes O1/O2/S0: 0 cudaHostAlloc,
+    PRNG_OPT_HOST_MEM = 8,     /* pinned host halves of modes O1/O2/S0: 0 cudaHostAlloc,
                                   1 write-combined, 2 THP-backed mmap + cudaHostRegister  */
+    PRNG_OPT_TRACE_PTR = 9     /* diagnostic: device pointer receiving %globaltimer stamps
+                                  [CTA][round][iteration / 64] from variant "v2n4s1t"      */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two

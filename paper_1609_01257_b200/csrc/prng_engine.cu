@@ -82,6 +82,8 @@ const Variant kVariants[] = {
     V("v4n8cs", 4, 8, 1, 0, 1, 0),    V("v2n8cs", 2, 8, 1, 0, 1, 0),
     // cluster barrier (split arrive / wait) every iteration (c2 ~ s1; c4 ~ 4.4 TB/s)
     V("v2n8c2", 2, 8, 0, 2, 2, 4),    V("v2n8c4", 2, 8, 0, 2, 4, 4),
+    // diagnostic: v2n4s1 + per-CTA %globaltimer trace (PRNG_OPT_TRACE_PTR)
+    V("v2n4s1t", 2, 4, 0, 3, 1, 4),
 };
 #undef V
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
@@ -126,6 +128,8 @@ struct prng {
     // options
     int mode = PRNG_MODE_OVERLAP2;
     int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0, ring_pad = 0;
+    unsigned long long *trace = nullptr;  // PRNG_OPT_TRACE_PTR (diagnostic variant only)
+
     int profile = 0, kernel = 0;
     int blocks_per_sm[kNumVariants] = {0};
 
@@ -228,6 +232,8 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     a.count = h->count;
     a.iters = iters;
     a.first_is_state = first_is_state ? 1u : 0u;
+    a.trace = h->trace;
+
     const uint64_t piece = 32ull * v.npt;
     a.npieces = (h->count + piece - 1) / piece;
     // Persistent grid: at most one wave of resident warps; equalise pieces per warp.
@@ -459,6 +465,10 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             if (value < HK_PINNED || value > HK_HUGE_REGISTERED) return set_err(err, PRNG_EINVAL, "bad host mem kind");
             h->host_mem = (int)value;
             break;
+        case PRNG_OPT_TRACE_PTR:
+            h->trace = (unsigned long long *)(uintptr_t)value;
+            break;
+
 
         default:
             return set_err(err, PRNG_EINVAL, "unknown option %d", option);
@@ -477,6 +487,8 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_GRID_WARPS: *value = h->grid_warps; break;
         case PRNG_OPT_RING_PAD: *value = h->ring_pad; break;
         case PRNG_OPT_HOST_MEM: *value = h->host_mem; break;
+        case PRNG_OPT_TRACE_PTR: *value = (int64_t)(uintptr_t)h->trace; break;
+
 
         default: return set_err(err, PRNG_EINVAL, "unknown option %d", option);
     }

@@ -138,6 +138,7 @@ struct BatchArgs {
                               //    emit the state unchanged, then step (A6)
     uint64_t npieces;         // ceil(count / (32 * NPT))
     uint32_t rounds;          // ceil(npieces / warps in grid)
+    unsigned long long *trace;  // SYNC 3 (diagnostic): %globaltimer per CTA, round, 64 iterations
 };
 
 // Warp coherence (SYNC):
@@ -149,6 +150,8 @@ struct BatchArgs {
 //            iteration's stores are issued, wait just before the next iteration's stores,
 //            so the xorshift arithmetic overlaps the barrier.  Warps without a piece in
 //            the last round still take part in the barriers (IDLE mode).
+//   3  as 1, plus a %globaltimer trace (diagnostic: measured CTA drift of ~180 iterations
+//            at numrn = 2^24, i.e. the grid writes ~180 ring slots at once).
 // Fewer drifting write streams -> fewer concurrently open DRAM pages.
 enum PieceMode { FULL = 0, PARTIAL = 1, IDLE = 2 };
 
@@ -158,7 +161,8 @@ __device__ __forceinline__ void cluster_arrive() {
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
 template <int VEC, int NPT, int POLICY, int SYNC, int MODE>
-__device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uint32_t bar_threads) {
+__device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uint32_t bar_threads,
+                                          uint32_t trace_round) {
     constexpr int NV = NPT / VEC;
     uint64_t x[NPT];
     // ---- load the NPT states of this lane (read once per launch)
@@ -200,7 +204,16 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uin
                 for (int e = 0; e < VEC; ++e)
                     if (base + (uint64_t)v * 32 * VEC + e < a.count) p[v * 32 * VEC + e] = x[v * VEC + e];
         }
-        if constexpr (SYNC == 1) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+        if constexpr (SYNC == 1 || SYNC == 3) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+        if constexpr (SYNC == 3) {
+            // drift diagnostic: CTA-leader timestamps every 64 iterations
+            if ((t & 63) == 0 && (threadIdx.x & 31) == 0 && bar_threads > 0 && a.trace && threadIdx.x == 0) {
+                unsigned long long ts;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+                const uint64_t per_round = (a.iters + 63) / 64;
+                a.trace[((uint64_t)blockIdx.x * a.rounds + trace_round) * per_round + (t >> 6)] = ts;
+            }
+        }
         if constexpr (SYNC == 2) cluster_arrive();
         // advance to the next slot of the ring (warp-uniform)
         if (++slot == a.nslots) {
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
         const uint64_t base = piece * PIECE + (uint64_t)lane * VEC;
         if (piece >= a.npieces) {  // warp-uniform
             if constexpr (SYNC == 2) {
-                run_piece<VEC, NPT, POLICY, SYNC, IDLE>(a, base, 0);
+                run_piece<VEC, NPT, POLICY, SYNC, IDLE>(a, base, 0, r);
                 continue;
             } else {
                 break;
@@ -250,9 +263,9 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
         const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
         const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - first < wpb ? a.npieces - first : wpb);
         if ((piece + 1) * PIECE <= a.count)
-            run_piece<VEC, NPT, POLICY, SYNC, FULL>(a, base, bar_threads);
+            run_piece<VEC, NPT, POLICY, SYNC, FULL>(a, base, bar_threads, r);
         else
-            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL>(a, base, bar_threads);
+            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL>(a, base, bar_threads, r);
     }
 }
 

@@ -14,8 +14,7 @@ timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench
 # ncu: the default variant (id 0) in bench.py's launch configuration, no autotune probes
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --kernel 0 --steps 2 --warmup 1 --no-e2e --no-cpu --no-probes > $OUT/ncu_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:batch_kernel -s 1 -c 1 \
-    -o $OUT/prof_batch python bench.py --kernel 0 --steps 1 --warmup 1 --no-e2e --no-cpu --no-probes > $OUT/ncu_full.log 2>&1
-timeout 600 ncu --metrics dram__bytes_write.sum,dram__bytes_read.sum,gpu__time_duration.sum --clock-control none --csv \
-    --log-file $OUT/dram_lin.csv python bench.py --kernel 0 --numiter 250 --steps 1 --warmup 1 --no-e2e --no-cpu --no-probes > /dev/null 2>&1
+# full section set: application replay (no 64 GiB save/restore per pass)
+timeout 1500 ncu --set full --clock-control none --import-source on --replay-mode application -k regex:batch_kernel -c 1 \
+    -o $OUT/prof_batch python tools/profile_step.py > $OUT/ncu_full.log 2>&1
 ls -la $OUT
