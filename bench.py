@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--numrn-total", type=int, default=0, help="strong scaling: fixed total numrn (e.g. 2^28)")
     ap.add_argument("--numiter", type=int, default=DEF_NUMITER)
     ap.add_argument("--seed", type=int, default=SEED_PERF)
-    ap.add_argument("--kernel", type=int, default=-1, help="kernel variant id (-1: prng_autotune picks)")
+    ap.add_argument("--kernel", type=int, default=0, help="kernel variant id (default 0 = v2n4s1; -1: prng_autotune)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--e2e-mode", type=int, default=3, help="0 S0, 1 S1, 2 O1, 3 O2")
@@ -227,7 +227,8 @@ def run_ours(a, D):
     P.prng_set_streams(h, gen.cuda_stream, cop.cuda_stream)
     P.prng_set_option(h, P.PRNG_OPT_MODE, a.e2e_mode)
     tune_gbs = None
-    if a.kernel < 0:  # untimed setup, like a library autotuner
+    if a.kernel < 0:  # untimed setup, like a library autotuner; off by default so
+        # the timed kernel is the one profiles/ holds the ncu capture of
         tune_gbs = P.prng_autotune(h)
     else:
         P.prng_set_option(h, P.PRNG_OPT_KERNEL, a.kernel)

@@ -66,9 +66,11 @@ struct Variant {
     int vec, npt, policy, sync, cluster;  // sync: 0 none, 1 CTA barrier, 2 cluster barrier
     int warps_per_sm;                     // default grid: resident warps per SM (0 = occupancy max)
     BatchFn fn;
+    int stages;                           // > 0: TMA bulk-store kernel with this many smem stages
 };
 #define V(name, vec, npt, pol, sync, cl, wps) \
-    {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>}
+    {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>, 0}
+#define VT(name, npt, stages, wps) {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages}
 // Measured on B200 at numrn = 2^24 x 1000 through a non-reused 64 GiB ring
 // (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 16-B vectors reach
 // ~6.9 TB/s (93 % of the same-box cudaMemset fill rate); free-running warps at full
@@ -84,9 +86,16 @@ const Variant kVariants[] = {
     V("v2n8c2", 2, 8, 0, 2, 2, 4),    V("v2n8c4", 2, 8, 0, 2, 4, 4),
     // diagnostic: v2n4s1 + per-CTA %globaltimer trace (PRNG_OPT_TRACE_PTR)
     V("v2n4s1t", 2, 4, 0, 3, 1, 4),
+    // TMA bulk stores: one cp.async.bulk per warp per iteration from an smem stage ring
+    VT("t2n4", 4, 4, 4),   VT("t2n8", 8, 4, 4),   VT("t2n16", 16, 4, 4),  VT("t2n8s8", 8, 8, 4),
+    VT("t2n4w8", 4, 4, 8), VT("t2n8w8", 8, 4, 8),
 };
+#undef VT
 #undef V
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+size_t variant_smem(const Variant &v, uint64_t warps_per_block) {
+    return v.stages ? (size_t)warps_per_block * v.stages * 32 * v.npt * sizeof(uint64_t) : 0;
+}
 constexpr int kBlock = 256;
 
 double now_s() {
@@ -282,7 +291,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
         cfg.numAttrs = 1;
         CU(cudaLaunchKernelEx(&cfg, v.fn, a));
     } else {
-        v.fn<<<(unsigned)blocks, (unsigned)(32 * wpb), 0, s>>>(a);
+        v.fn<<<(unsigned)blocks, (unsigned)(32 * wpb), variant_smem(v, wpb), s>>>(a);
     }
     CU(cudaGetLastError());
     return prof_end(h, s, err);
@@ -370,7 +379,12 @@ prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begi
         return bail("cudaDeviceGetAttribute(SMs)", e);
     cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, dev);
     for (int i = 0; i < kNumVariants; ++i) {
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm[i], kVariants[i].fn, kBlock, 0)) !=
+        const size_t smem = variant_smem(kVariants[i], kBlock / 32);
+        if (smem > 48 * 1024 &&
+            (e = cudaFuncSetAttribute(kVariants[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+                cudaSuccess)
+            return bail("cudaFuncSetAttribute(smem)", e);
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm[i], kVariants[i].fn, kBlock, smem)) !=
             cudaSuccess)
             return bail("cudaOccupancyMaxActiveBlocksPerMultiprocessor", e);
         if (h->blocks_per_sm[i] < 1) h->blocks_per_sm[i] = 1;
@@ -610,7 +624,7 @@ static const struct {
     const char *variant;
     int warps_per_sm;
 } kTuneCandidates[] = {{"v2n4s1", 4}, {"v2n4s1", 8}, {"v2n8s1", 4}, {"v2n8s1", 8},
-                       {"v2n16s1", 4}, {"v2n8c2", 4}, {"v4n8s1", 4}, {"v2n8", 4}};
+                       {"v2n16s1", 4}, {"v2n8c2", 4}, {"v4n8s1", 4}, {"t2n8w8", 8}};
 
 extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err) {
     if (int rc = check_handle(h, err, false)) return rc;

@@ -269,6 +269,77 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- a2+a3 with TMA bulk stores
+// Same work decomposition (VEC = 2), but each iteration's piece is staged in shared
+// memory (STS.128, same lane layout) and written to HBM by ONE bulk async copy per warp
+// (cp.async.bulk.global.shared::cta, 32*NPT*8 contiguous bytes): the SMs issue 1 store
+// instruction per piece instead of NPT/2, the copy engine of the SM forms the DRAM bursts.
+// A ring of STAGES smem buffers per warp lets STAGES-1 bulk copies stay in flight; lane 0
+// waits (wait_group.read) before its stage is overwritten.  Partial pieces fall back to
+// the predicated STG path.
+template <int NPT, int STAGES>
+__device__ __forceinline__ void run_piece_tma(const BatchArgs &a, uint64_t piece, uint32_t lane, uint64_t *wbuf) {
+    constexpr int NV = NPT / 2;
+    constexpr uint32_t BYTES = 32u * NPT * 8u;
+    const uint64_t base = piece * 32ull * NPT + 2ull * lane;
+    uint64_t x[NPT];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) load_vec<2>(a.state + base + (uint64_t)v * 64, x + 2 * v);
+    uint64_t *g = a.dst + (uint64_t)a.slot0 * a.pitch + piece * 32ull * NPT;
+    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
+    uint32_t slot = a.slot0;
+    for (uint32_t t = 0; t < a.iters; ++t) {
+        if (t > 0 || !a.first_is_state) {
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
+        }
+        uint64_t *sb = wbuf + (t % STAGES) * (32 * NPT);
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(STAGES - 1) : "memory");
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sb + v * 64 + 2 * lane);
+            asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa), "l"(x[2 * v]), "l"(x[2 * v + 1]) : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sb);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa), "n"(BYTES)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (++slot == a.nslots) {
+            slot = 0;
+            g -= wrap;
+        } else {
+            g += a.pitch;
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) store_vec<2, 0>(a.state + base + (uint64_t)v * 64, x + 2 * v);
+}
+
+template <int NPT, int STAGES>
+__global__ void __launch_bounds__(256) batch_kernel_tma(BatchArgs a) {
+    extern __shared__ __align__(128) uint64_t smem_tma[];
+    constexpr uint64_t PIECE = 32ull * NPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t wib = threadIdx.x >> 5;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t *wbuf = smem_tma + (uint64_t)wib * STAGES * PIECE;
+    for (uint32_t r = 0; r < a.rounds; ++r) {
+        const uint64_t piece = (uint64_t)r * nwarps + warp;
+        if (piece >= a.npieces) break;  // warp-uniform
+        if ((piece + 1) * PIECE <= a.count)
+            run_piece_tma<NPT, STAGES>(a, piece, lane, wbuf);
+        else
+            run_piece<2, NPT, 0, 0, PARTIAL>(a, piece * PIECE + 2ull * lane, 0, r);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- roofline probe kernel
 // Pure 32-byte streaming store of a constant pattern: the same-box write ceiling.
 __global__ void __launch_bounds__(256) store_probe_kernel(uint64_t *p, uint64_t n4) {
