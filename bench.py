@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--no-probes", action="store_true")
     ap.add_argument("--cpu-numiter", type=int, default=64, help="oracle sample: numiter at full numrn")
     ap.add_argument("--ref-numiter", type=int, default=8, help="--impl reference: numiter per step sample")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--device-mod", type=int, default=0,
+                    help="TEST ONLY: map local rank r to GPU r %% K (several ranks per GPU; timings meaningless)")
     return ap.parse_args()
 
 
@@ -218,12 +221,13 @@ def run_ours(a, D):
     import torch
     import paper_1609_01257_b200 as P
 
-    torch.cuda.set_device(D.local)
+    dev = D.local % a.device_mod if a.device_mod > 0 else D.local
+    torch.cuda.set_device(dev)
     numrn = a.numrn_total or a.numrn_per_gpu * D.world
     gb, cnt = shard_range(numrn, D.rank, D.world)
     gen = torch.cuda.Stream()
     cop = torch.cuda.Stream()
-    h = P.prng_create_range(numrn, a.seed, gb, cnt, D.local)
+    h = P.prng_create_range(numrn, a.seed, gb, cnt, dev)
     P.prng_set_streams(h, gen.cuda_stream, cop.cuda_stream)
     P.prng_set_option(h, P.PRNG_OPT_MODE, a.e2e_mode)
     tune_gbs = None
@@ -242,7 +246,7 @@ def run_ours(a, D):
     P.prng_set_option(h, P.PRNG_OPT_PROFILE, 1)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kern_ms, init_ms, launches = [], [], 0
-    with Clocks(D.local) as clk:
+    with Clocks(dev) as clk:
         D.barrier()
         torch.cuda.synchronize()
         ev0.record(gen)
@@ -354,7 +358,7 @@ def run_ours(a, D):
 
 def main():
     a = parse()
-    D = Dist(None if a.impl == "reference" else "nccl")
+    D = Dist(None if a.impl == "reference" else a.dist_backend)
     try:
         if a.impl == "reference":
             run_reference(a, D)

@@ -200,6 +200,35 @@ int prng_prof_calc(uint64_t nevents, const uint32_t *name_id, const double *star
                    const double *end_s, uint32_t nnames, double elapsed, double *agg_abs,
                    double *overlap, double *effective, double *elapsed_out, prng_err_t *err);
 
+/* Sort flags of the summary, after cf4ocl's (CCL_PROF_AGG_SORT_TIME |
+ * CCL_PROF_SORT_DESC, CCL_PROF_OVERLAP_SORT_DURATION | CCL_PROF_SORT_DESC). */
+#define PRNG_PROF_AGG_SORT_NAME 0x0
+#define PRNG_PROF_AGG_SORT_TIME 0x1
+#define PRNG_PROF_OVERLAP_SORT_NAME 0x0
+#define PRNG_PROF_OVERLAP_SORT_DURATION 0x1
+#define PRNG_PROF_SORT_ASC 0x0
+#define PRNG_PROF_SORT_DESC 0x10
+
+/* NEXT-2: the text summary of cf4ocl's ccl_prof_get_summary in the layout of Fig. 3
+ * (P:297-321): aggregate table (name, relative %, absolute s), event-overlap table,
+ * "Tot. of all events (eff.)", "Total ellapsed time" (sic, as printed), device and host
+ * shares.  names[nnames] are the event names (NULL = prng_event_name(id)); only names
+ * that occur are listed; zero overlaps are omitted.  Writes a NUL-terminated string into
+ * buf (cap bytes); *len (may be NULL) gets the full length, PRNG_EINVAL if cap is short. */
+int prng_prof_summary(uint64_t nevents, const uint32_t *name_id, const double *start_s,
+                      const double *end_s, uint32_t nnames, const char *const *names, double elapsed,
+                      int agg_sort, int overlap_sort, char *buf, uint64_t cap, uint64_t *len,
+                      prng_err_t *err);
+
+/* NEXT-2: the profiler's export table: one line per event,
+ * "queue<TAB>start_ns<TAB>end_ns<TAB>event name", sorted by (start, end, queue), LF line
+ * endings, written to `path`.  queues[nnames] name the queue of each event name (NULL =
+ * "Main" for kernels, "Comms" for READ_BUFFER, "Host" for OUT).  For ccl_plot_events-style
+ * charts (tools/plot_events.py, Fig. 5). */
+int prng_prof_export(uint64_t nevents, const uint32_t *name_id, const double *start_s,
+                     const double *end_s, uint32_t nnames, const char *const *names,
+                     const char *const *queues, const char *path, prng_err_t *err);
+
 /* ------------------------------------------------------------------ roofline probes */
 /* Same-box denominators: each returns GB/s (best of `reps`) or < 0 on
  * error.  bytes: buffer size. */

@@ -97,6 +97,8 @@ def lib():
         "prng_event_name": ([u32], ctypes.c_char_p),
         "prng_prof_events": ([vp, u64, vp, vp, vp, P64, PD, E], i32),
         "prng_prof_calc": ([u64, vp, vp, vp, u32, dbl, vp, vp, PD, PD, E], i32),
+        "prng_prof_summary": ([u64, vp, vp, vp, u32, vp, dbl, i32, i32, vp, u64, P64, E], i32),
+        "prng_prof_export": ([u64, vp, vp, vp, u32, vp, vp, ctypes.c_char_p, E], i32),
         "prng_probe_memset_gbs": ([u64, i32], dbl),
         "prng_probe_store_gbs": ([u64, i32], dbl),
         "prng_probe_d2h_gbs": ([u64, i32, i32, i32], dbl),
@@ -279,6 +281,50 @@ def prng_prof_calc(name_id, start_s, end_s, nnames: int = 4, elapsed: float = 0.
     _check(lib().prng_prof_calc(len(ids), _ptr(ids), _ptr(s), _ptr(e), nnames, elapsed, _ptr(agg), _ptr(ov),
                                 ctypes.byref(eff), ctypes.byref(el), ctypes.byref(err)), err)
     return {"agg": agg, "overlap": ov, "effective": eff.value, "elapsed": el.value}
+
+
+PRNG_PROF_AGG_SORT_NAME, PRNG_PROF_AGG_SORT_TIME = 0x0, 0x1
+PRNG_PROF_OVERLAP_SORT_NAME, PRNG_PROF_OVERLAP_SORT_DURATION = 0x0, 0x1
+PRNG_PROF_SORT_ASC, PRNG_PROF_SORT_DESC = 0x0, 0x10
+
+
+def _names_arg(names, nnames):
+    if names is None:
+        return None, None
+    arr = (ctypes.c_char_p * nnames)(*[n.encode() if n is not None else None for n in names])
+    return arr, arr
+
+
+def prng_prof_summary(name_id, start_s, end_s, nnames: int = 4, names=None, elapsed: float = 0.0,
+                      agg_sort: int = PRNG_PROF_AGG_SORT_TIME | PRNG_PROF_SORT_DESC,
+                      overlap_sort: int = PRNG_PROF_OVERLAP_SORT_DURATION | PRNG_PROF_SORT_DESC) -> str:
+    """Fig. 3-layout summary text."""
+    ids = np.ascontiguousarray(name_id, dtype=np.uint32)
+    s = np.ascontiguousarray(start_s, dtype=np.float64)
+    e = np.ascontiguousarray(end_s, dtype=np.float64)
+    arr, keep = _names_arg(names, nnames)
+    n = u64()
+    err = prng_err_t()
+    lib().prng_prof_summary(len(ids), _ptr(ids), _ptr(s), _ptr(e), nnames, arr, elapsed, agg_sort, overlap_sort,
+                            None, 0, ctypes.byref(n), ctypes.byref(err))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _check(lib().prng_prof_summary(len(ids), _ptr(ids), _ptr(s), _ptr(e), nnames, arr, elapsed, agg_sort,
+                                   overlap_sort, buf, n.value + 1, ctypes.byref(n), ctypes.byref(err)), err)
+    del keep
+    return buf.value.decode()
+
+
+def prng_prof_export(path: str, name_id, start_s, end_s, nnames: int = 4, names=None, queues=None) -> None:
+    """Export table: queue, start ns, end ns, event name (tab-separated)."""
+    ids = np.ascontiguousarray(name_id, dtype=np.uint32)
+    s = np.ascontiguousarray(start_s, dtype=np.float64)
+    e = np.ascontiguousarray(end_s, dtype=np.float64)
+    narr, k1 = _names_arg(names, nnames)
+    qarr, k2 = _names_arg(queues, nnames)
+    err = prng_err_t()
+    _check(lib().prng_prof_export(len(ids), _ptr(ids), _ptr(s), _ptr(e), nnames, narr, qarr, path.encode(),
+                                  ctypes.byref(err)), err)
+    del k1, k2
 
 
 def prng_probe_memset_gbs(nbytes: int, reps: int = 5) -> float:

@@ -30,8 +30,30 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
+CLI_SRC = os.path.join(CSRC, "rng_cli.c")
+CLI = os.path.join(PKG, "bin", "rng_b200")
+
+
+def build_cli(force: bool = False) -> str:
+    """The paper's example program (NEXT-1), linked against libprng_b200.so."""
+    if not force and os.path.exists(CLI) and os.path.getmtime(CLI) >= max(
+            os.path.getmtime(CLI_SRC), os.path.getmtime(LIB), os.path.getmtime(os.path.join(ROOT, "include", "prng.h"))):
+        return CLI
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    tmp = CLI + f".tmp{os.getpid()}"
+    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-D_POSIX_C_SOURCE=200809L", "-I", os.path.join(ROOT, "include"),
+           "-o", tmp, CLI_SRC, "-L", PKG, "-l:libprng_b200.so", "-Wl,-rpath,$ORIGIN/.."]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"gcc failed ({r.returncode}): {' '.join(cmd)}")
+    os.replace(tmp, CLI)
+    return CLI
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
+        build_cli()
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
@@ -44,6 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(r.stderr)
     os.replace(tmp, LIB)
+    build_cli(force=True)
     return LIB
 
 

@@ -11,6 +11,9 @@
 // to (a, a); the union gains L when any event is active.  O(E log E + S * nnames^2),
 // versus the O(E^2) pair loop the paper calls "computationally expensive".
 #include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <string>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -84,6 +87,146 @@ extern "C" int prng_prof_calc(uint64_t nevents, const uint32_t *name_id, const d
         active += pts[i].delta;
     }
     *elapsed_out = elapsed > 0 ? elapsed : (nevents ? tmax - tmin : 0.0);
+    if (err) {
+        err->code = PRNG_OK;
+        err->msg[0] = 0;
+    }
+    return PRNG_OK;
+}
+
+// ---------------------------------------------------------------------------- summary (NEXT-2)
+// ccl_prof_get_summary's layout, as printed in Fig. 3.  The figure's header
+// line is cut at "Rel. time ("; it is read as "Rel. time (%)" / "Abs. time (s)"
+// (A17).  "ellapsed" is spelled as printed.
+namespace {
+struct Appender {
+    std::string s;
+    void f(const char *fmt, ...) {
+        char tmp[512];
+        va_list ap;
+        va_start(ap, fmt);
+        std::vsnprintf(tmp, sizeof(tmp), fmt, ap);
+        va_end(ap);
+        s += tmp;
+    }
+};
+const char *name_of(const char *const *names, uint32_t i) { return (names && names[i]) ? names[i] : prng_event_name(i); }
+}  // namespace
+
+extern "C" int prng_prof_summary(uint64_t nevents, const uint32_t *name_id, const double *start_s,
+                                 const double *end_s, uint32_t nnames, const char *const *names, double elapsed,
+                                 int agg_sort, int overlap_sort, char *buf, uint64_t cap, uint64_t *len,
+                                 prng_err_t *err) {
+    std::vector<double> agg(nnames ? nnames : 1), ov((size_t)(nnames ? nnames : 1) * (nnames ? nnames : 1));
+    double eff = 0, el = 0;
+    if (int rc = prng_prof_calc(nevents, name_id, start_s, end_s, nnames, elapsed, agg.data(), ov.data(), &eff, &el,
+                                err))
+        return rc;
+    std::vector<char> seen(nnames, 0);
+    for (uint64_t i = 0; i < nevents; ++i) seen[name_id[i]] = 1;
+    double total = 0;
+    std::vector<uint32_t> ids;
+    for (uint32_t i = 0; i < nnames; ++i)
+        if (seen[i]) {
+            ids.push_back(i);
+            total += agg[i];
+        }
+    const bool adesc = agg_sort & PRNG_PROF_SORT_DESC, aby_time = agg_sort & PRNG_PROF_AGG_SORT_TIME;
+    std::stable_sort(ids.begin(), ids.end(), [&](uint32_t x, uint32_t y) {
+        if (aby_time) return adesc ? agg[x] > agg[y] : agg[x] < agg[y];
+        const int c = std::strcmp(name_of(names, x), name_of(names, y));
+        return adesc ? c > 0 : c < 0;
+    });
+    Appender o;
+    const char *rule = "   ------------------------------------------------------------------\n";
+    o.f(" Aggregate times by event  :\n");
+    o.s += rule;
+    o.f("   | %-30s | %13s | %13s |\n", "Event name", "Rel. time (%)", "Abs. time (s)");
+    o.s += rule;
+    for (uint32_t i : ids)
+        o.f("   | %-30s | %13.4f | %13.4e |\n", name_of(names, i), total > 0 ? 100.0 * agg[i] / total : 0.0, agg[i]);
+    o.s += rule;
+    o.f("                                    | %13s | %13.4e |\n", "Total", total);
+    o.f("                                    ---------------------------------\n");
+    struct Pair {
+        uint32_t a, b;
+        double v;
+    };
+    std::vector<Pair> pairs;
+    double ovt = 0;
+    for (uint32_t a = 0; a < nnames; ++a)
+        for (uint32_t b = a; b < nnames; ++b)
+            if (ov[(size_t)a * nnames + b] > 0) {
+                pairs.push_back({a, b, ov[(size_t)a * nnames + b]});
+                ovt += ov[(size_t)a * nnames + b];
+            }
+    const bool odesc = overlap_sort & PRNG_PROF_SORT_DESC, oby_dur = overlap_sort & PRNG_PROF_OVERLAP_SORT_DURATION;
+    std::stable_sort(pairs.begin(), pairs.end(), [&](const Pair &x, const Pair &y) {
+        if (oby_dur) return odesc ? x.v > y.v : x.v < y.v;
+        int c = std::strcmp(name_of(names, x.a), name_of(names, y.a));
+        if (!c) c = std::strcmp(name_of(names, x.b), name_of(names, y.b));
+        return odesc ? c > 0 : c < 0;
+    });
+    if (!pairs.empty()) {
+        o.f(" Event overlaps            :\n");
+        o.s += rule;
+        o.f("   | %-22s | %-22s | %-12s |\n", "Event 1", "Event2", "Overlap (s)");
+        o.s += rule;
+        for (const auto &p : pairs) o.f("   | %-22s | %-22s | %12.4e |\n", name_of(names, p.a), name_of(names, p.b), p.v);
+        o.s += rule;
+        o.f("                            | %22s | %12.4e |\n", "Total", ovt);
+        o.f("                            -----------------------------------------\n");
+    }
+    o.f(" Tot. of all events (eff.) : %es\n", eff);
+    o.f(" Total ellapsed time       : %es\n", el);
+    const double dev = el > 0 ? eff / el : 0.0;
+    o.f(" Time spent in device      : %.2f%%\n", 100.0 * dev);
+    o.f(" Time spent in host        : %.2f%%\n", 100.0 * (1.0 - dev));
+    if (len) *len = o.s.size();
+    if (!buf || cap < o.s.size() + 1) {
+        if (err) {
+            err->code = PRNG_EINVAL;
+            std::snprintf(err->msg, sizeof(err->msg), "summary needs %zu bytes", o.s.size() + 1);
+        }
+        return PRNG_EINVAL;
+    }
+    std::memcpy(buf, o.s.c_str(), o.s.size() + 1);
+    if (err) {
+        err->code = PRNG_OK;
+        err->msg[0] = 0;
+    }
+    return PRNG_OK;
+}
+
+// ---------------------------------------------------------------------------- export (NEXT-2)
+extern "C" int prng_prof_export(uint64_t nevents, const uint32_t *name_id, const double *start_s,
+                                const double *end_s, uint32_t nnames, const char *const *names,
+                                const char *const *queues, const char *path, prng_err_t *err) {
+    if (!path || (nevents && (!name_id || !start_s || !end_s))) return fail(err, PRNG_EINVAL, "prng_prof_export: NULL");
+    struct Row {
+        long long a, b;
+        std::string q, n;
+    };
+    std::vector<Row> rows;
+    for (uint64_t i = 0; i < nevents; ++i) {
+        const uint32_t id = name_id[i];
+        if (id >= nnames) return fail(err, PRNG_EINVAL, "prng_prof_export: name id out of range");
+        const char *q = (queues && queues[id]) ? queues[id]
+                        : id == PRNG_EV_READ_BUFFER ? "Comms"
+                        : id == PRNG_EV_OUT         ? "Host"
+                                                    : "Main";
+        rows.push_back({std::llround(start_s[i] * 1e9), std::llround(end_s[i] * 1e9), q, name_of(names, id)});
+    }
+    std::stable_sort(rows.begin(), rows.end(), [](const Row &x, const Row &y) {
+        if (x.a != y.a) return x.a < y.a;
+        if (x.b != y.b) return x.b < y.b;
+        return x.q < y.q;
+    });
+    FILE *f = std::fopen(path, "w");
+    if (!f) return fail(err, PRNG_EINVAL, "prng_prof_export: cannot open file");
+    for (const auto &r : rows) std::fprintf(f, "%s\t%lld\t%lld\t%s\n", r.q.c_str(), r.a, r.b, r.n.c_str());
+    const bool bad = std::fclose(f) != 0;
+    if (bad) return fail(err, PRNG_EINVAL, "prng_prof_export: write failed");
     if (err) {
         err->code = PRNG_OK;
         err->msg[0] = 0;
