@@ -10,7 +10,8 @@ register-resident state, 32-byte stores into a device ring).  BASELINE.json's me
 random numbers/s (and GB/s, 8 B per number, Eq. 1) device-only and end to end.
 
 * value      device-only numbers/s over all ranks: inputs (numrn, numiter, seed) resident,
-             output ring (>= 2 GiB, > 16x the 126 MB L2, so no L2 flush is needed) in HBM.
+             output through a 64 GiB rotating ring in HBM (no address rewritten within
+             64 GiB, > 500x the 126 MB L2, so no L2 flush is needed).
              Timed with CUDA events on the generation stream (a torch stream handed to the
              library), K steps between barrier + synchronize, max over ranks.
 * e2e        same metric through the C-ABI call with HOST buffers: prng_generate with the
@@ -65,6 +66,7 @@ def parse():
     ap.add_argument("--cpu-numiter", type=int, default=64, help="oracle sample: numiter at full numrn")
     ap.add_argument("--ref-numiter", type=int, default=8, help="--impl reference: numiter per step sample")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--output", type=int, default=0, help="0 = the state (paper); 1 = xorshift64* scrambled (NEXT-3)")
     ap.add_argument("--device-mod", type=int, default=0,
                     help="TEST ONLY: map local rank r to GPU r %% K (several ranks per GPU; timings meaningless)")
     return ap.parse_args()
@@ -189,6 +191,24 @@ def cpu_baseline(numrn, numiter, seed):
     return numrn * numiter / dt, dt
 
 
+def cpu_baseline_all_cores(numrn, numiter, seed):
+    """The same oracle function, unchanged, on one contiguous gid shard per host core
+    (threads: ctypes releases the GIL), as BASELINE.md's CPU plan asks."""
+    import threading
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    oracle.lib()
+    shards = [shard_range(numrn, r, cores) for r in range(cores)]
+    th = [threading.Thread(target=oracle.digest, args=(numrn, numiter, seed, b, c)) for b, c in shards if c]
+    t = time.perf_counter()
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    dt = time.perf_counter() - t
+    return numrn * numiter / dt, dt, len(th)
+
+
 def run_reference(a, D):
     """--impl reference: the oracle as it stands, on the host cores, rank 0 only."""
     if D.rank != 0:
@@ -230,6 +250,7 @@ def run_ours(a, D):
     h = P.prng_create_range(numrn, a.seed, gb, cnt, dev)
     P.prng_set_streams(h, gen.cuda_stream, cop.cuda_stream)
     P.prng_set_option(h, P.PRNG_OPT_MODE, a.e2e_mode)
+    P.prng_set_option(h, P.PRNG_OPT_OUTPUT, a.output)
     tune_gbs = None
     if a.kernel < 0:  # untimed setup, like a library autotuner; off by default so
         # the timed kernel is the one profiles/ holds the ncu capture of
@@ -337,6 +358,10 @@ def run_ours(a, D):
         v, dt = cpu_baseline(numrn, a.cpu_numiter, a.seed)
         cpu = {"value": v, "unit": "numbers/s", "cores": 1, "kind": "oracle",
                "sample": f"numrn={numrn} x numiter={a.cpu_numiter} ({dt:.1f} s, digest-folded, 1 thread)"}
+        va, dta, nth = cpu_baseline_all_cores(numrn, 4 * a.cpu_numiter, a.seed)
+        cpu["all_cores"] = {"value": va, "unit": "numbers/s", "cores": nth,
+                            "sample": f"numrn={numrn} x numiter={4 * a.cpu_numiter} ({dta:.1f} s), one gid shard "
+                                      f"per thread"}
 
     if D.rank == 0:
         line = {
@@ -349,6 +374,7 @@ def run_ours(a, D):
                                     f" x numiter={a.numiter}, device-only" if D.world == 1 else
                                     f"numrn={numrn} total ({cnt} per GPU, gid-range sharded) x numiter={a.numiter}"),
                        "numrn": numrn, "numiter": a.numiter, "seed": a.seed, "parallelism": f"gid-shard{D.world}",
+                       "output": ["state (paper)", "xorshift64* scrambled"][a.output],
                        "l2": "output through a 64 GiB rotating ring per GPU (> 500x L2; no address rewritten "
                              "within 64 GiB, see profiles/r1_ring_absorption.md); no flush needed"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -139,8 +139,11 @@ enum prng_option {
                                   of 4; breaks power-of-two slot strides); default 0       */
     PRNG_OPT_HOST_MEM = 8,     /* pinned host halves of modes O1/O2/S0: 0 cudaHostAlloc,
                                   1 write-combined, 2 THP-backed mmap + cudaHostRegister  */
-    PRNG_OPT_TRACE_PTR = 9     /* diagnostic: device pointer receiving %globaltimer stamps
+    PRNG_OPT_TRACE_PTR = 9,    /* diagnostic: device pointer receiving %globaltimer stamps
                                   [CTA][round][iteration / 64] from variant "v2n4s1t"      */
+    PRNG_OPT_OUTPUT = 10       /* NEXT-3 output transform: 0 = the state (the paper, A7);
+                                  1 = state * 0x2545F4914F6CDD1D mod 2^64 (xorshift64*-style
+                                  scrambler, A19).  Needs kernel variant 0..3.              */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two

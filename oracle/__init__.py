@@ -47,6 +47,8 @@ def lib():
         L.orc_sample.argtypes, L.orc_sample.restype = [u32, u64, u64], u64
         L.orc_stream.argtypes, L.orc_stream.restype = [u64, u64, u64, u64, u64, p64], i32
         L.orc_digest.argtypes, L.orc_digest.restype = [u64, u64, u64, u64, u64, p64, p64], i32
+        L.orc_star.argtypes, L.orc_star.restype = [u64], u64
+        L.orc_stream_star.argtypes, L.orc_stream_star.restype = [u64, u64, u64, u64, u64, p64], i32
         _lib = L
     return _lib
 
@@ -102,3 +104,19 @@ def digest(numrn: int, numiter: int, seed: int = 0, gid_begin: int = 0, count: i
     if rc != 0:
         raise ValueError(f"orc_digest rc={rc}")
     return x, s
+
+
+def star(x: int) -> int:
+    """NEXT-3 output scrambler (A19): x * 0x2545F4914F6CDD1D mod 2^64."""
+    return lib().orc_star(x & 0xFFFFFFFFFFFFFFFF)
+
+
+def stream_star(numrn: int, numiter: int, seed: int = 0, gid_begin: int = 0, count: int | None = None) -> np.ndarray:
+    """NEXT-3: the scrambled stream, shape [numiter, count] uint64."""
+    if count is None:
+        count = numrn - gid_begin
+    out = np.empty((numiter, count), dtype=np.uint64)
+    rc = lib().orc_stream_star(numrn, numiter, seed & 0xFFFFFFFFFFFFFFFF, gid_begin, count, _p64(out))
+    if rc != 0:
+        raise ValueError(f"orc_stream_star rc={rc}")
+    return out

@@ -165,3 +165,36 @@ int orc_digest(uint64_t numrn, uint64_t numiter, uint64_t seed,
     free(s);
     return ORC_OK;
 }
+
+/* NEXT-3 / A19: xorshift64*-style output scrambling on the same recurrence -- the emitted
+ * value is the state times Vigna's xorshift64* multiplier M32 = 2685821657736338717
+ * (0x2545F4914F6CDD1D), mod 2^64; P:177 (limitation 1) and P:358 ("a more complex PRNG
+ * could probably be used instead").  Same flat loop as orc_stream. */
+#define ORC_STAR_MUL 0x2545F4914F6CDD1Dull
+
+uint64_t orc_star(uint64_t x) { return x * ORC_STAR_MUL; }
+
+int orc_stream_star(uint64_t numrn, uint64_t numiter, uint64_t seed, uint64_t gid_begin, uint64_t count,
+                    uint64_t *out)
+{
+    int rc = orc_check(numrn, numiter, gid_begin, count);
+    if (rc != ORC_OK)
+        return rc;
+    if (count == 0)
+        return ORC_OK;
+    uint64_t *s = (uint64_t *)malloc(count * sizeof(uint64_t));
+    if (!s)
+        return ORC_ENOMEM;
+    for (uint64_t k = 0; k < numiter; ++k) {
+        for (uint64_t j = 0; j < count; ++j) {
+            uint32_t g = (uint32_t)(gid_begin + j);
+            if (k == 0)
+                s[j] = orc_seed64(g, seed);
+            else
+                s[j] = orc_xorshift64(s[j]);
+            out[k * count + j] = orc_star(s[j]);
+        }
+    }
+    free(s);
+    return ORC_OK;
+}

@@ -93,6 +93,12 @@ const Variant kVariants[] = {
 #undef VT
 #undef V
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+// NEXT-3: the CTA-synchronised variants (ids 0..3) instantiated with the xorshift64*
+// output scrambler (PRNG_OPT_OUTPUT = 1), same grid policy.
+const BatchFn kStarFns[] = {prngk::batch_kernel<2, 4, 0, 1, 1>, prngk::batch_kernel<2, 8, 0, 1, 1>,
+                            prngk::batch_kernel<2, 16, 0, 1, 1>, prngk::batch_kernel<4, 8, 0, 1, 1>};
+constexpr int kNumStar = sizeof(kStarFns) / sizeof(kStarFns[0]);
+
 size_t variant_smem(const Variant &v, uint64_t warps_per_block) {
     return v.stages ? (size_t)warps_per_block * v.stages * 32 * v.npt * sizeof(uint64_t) : 0;
 }
@@ -139,7 +145,7 @@ struct prng {
     int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0, ring_pad = 0;
     unsigned long long *trace = nullptr;  // PRNG_OPT_TRACE_PTR (diagnostic variant only)
 
-    int profile = 0, kernel = 0;
+    int profile = 0, kernel = 0, output = 0;
     int blocks_per_sm[kNumVariants] = {0};
 
     // profiling (a6)
@@ -231,7 +237,12 @@ int prof_end(prng *h, cudaStream_t s, prng_err_t *err) {
 // Launch one batch of `iters` iterations (a2 + a3) into dst slots.
 int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64_t slot0, uint32_t iters,
                  bool first_is_state, cudaStream_t s, prng_err_t *err) {
-    const Variant &v = kVariants[h->kernel];
+    const Variant &v0 = kVariants[h->kernel];
+    Variant v = v0;
+    if (h->output == 1) {
+        if (h->kernel >= kNumStar) return set_err(err, PRNG_EINVAL, "output scrambling needs kernel variant < %d", kNumStar);
+        v.fn = kStarFns[h->kernel];
+    }
     prngk::BatchArgs a;
     a.dst = dst;
     a.pitch = pitch;
@@ -465,7 +476,15 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             break;
         case PRNG_OPT_KERNEL:
             if (value < 0 || value >= kNumVariants) return set_err(err, PRNG_EINVAL, "bad kernel variant");
+            if (h->output == 1 && value >= kNumStar)
+                return set_err(err, PRNG_EINVAL, "output scrambling needs kernel variant < %d", kNumStar);
             h->kernel = (int)value;
+            break;
+        case PRNG_OPT_OUTPUT:
+            if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad output transform");
+            if (value == 1 && h->kernel >= kNumStar)
+                return set_err(err, PRNG_EINVAL, "output scrambling needs kernel variant < %d", kNumStar);
+            h->output = (int)value;
             break;
         case PRNG_OPT_GRID_WARPS:
             if (value < 0) return set_err(err, PRNG_EINVAL, "bad grid warps");
@@ -498,6 +517,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_RING_SLOTS: *value = h->ring_slots_opt; break;
         case PRNG_OPT_PROFILE: *value = h->profile; break;
         case PRNG_OPT_KERNEL: *value = h->kernel; break;
+        case PRNG_OPT_OUTPUT: *value = h->output; break;
         case PRNG_OPT_GRID_WARPS: *value = h->grid_warps; break;
         case PRNG_OPT_RING_PAD: *value = h->ring_pad; break;
         case PRNG_OPT_HOST_MEM: *value = h->host_mem; break;

@@ -60,6 +60,19 @@ __device__ __forceinline__ uint64_t xorshift64(uint64_t x) {
     return x;
 }
 
+// NEXT-3 (P:177 limitation 1, "a more complex PRNG could probably be used"):
+// optional xorshift64*-style output scrambling -- the emitted value is the state times
+// Vigna's xorshift64* multiplier (mod 2^64); the state recurrence is unchanged (DESIGN.md
+// A19).  One 64-bit multiply per number on the otherwise idle FMA pipe.
+constexpr uint64_t kStarMul = 0x2545F4914F6CDD1Dull;
+template <int OUT>
+__device__ __forceinline__ uint64_t emit(uint64_t x) {
+    if constexpr (OUT == 1)
+        return x * kStarMul;
+    else
+        return x;
+}
+
 // ---------------------------------------------------------------- vector memory helpers
 // POLICY 0: default write-back; 1: .cs (streaming, evict-first) -- the output is never
 // re-read by the SMs, only by the copy engine.
@@ -160,7 +173,7 @@ __device__ __forceinline__ void cluster_arrive() {
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
-template <int VEC, int NPT, int POLICY, int SYNC, int MODE>
+template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0>
 __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uint32_t bar_threads,
                                           uint32_t trace_round) {
     constexpr int NV = NPT / VEC;
@@ -196,13 +209,22 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uin
         }
         if constexpr (MODE == FULL) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) store_vec<VEC, POLICY>(p + v * 32 * VEC, x + v * VEC);
+            for (int v = 0; v < NV; ++v) {
+                if constexpr (OUT == 0) {
+                    store_vec<VEC, POLICY>(p + v * 32 * VEC, x + v * VEC);
+                } else {
+                    uint64_t y[VEC];
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) y[e] = emit<OUT>(x[v * VEC + e]);
+                    store_vec<VEC, POLICY>(p + v * 32 * VEC, y);
+                }
+            }
         } else if constexpr (MODE == PARTIAL) {
 #pragma unroll
             for (int v = 0; v < NV; ++v)
 #pragma unroll
                 for (int e = 0; e < VEC; ++e)
-                    if (base + (uint64_t)v * 32 * VEC + e < a.count) p[v * 32 * VEC + e] = x[v * VEC + e];
+                    if (base + (uint64_t)v * 32 * VEC + e < a.count) p[v * 32 * VEC + e] = emit<OUT>(x[v * VEC + e]);
         }
         if constexpr (SYNC == 1 || SYNC == 3) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
         if constexpr (SYNC == 3) {
@@ -239,7 +261,7 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uin
     }
 }
 
-template <int VEC, int NPT, int POLICY, int SYNC>
+template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0>
 __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
     constexpr uint64_t PIECE = 32ull * NPT;
@@ -253,7 +275,7 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
         const uint64_t base = piece * PIECE + (uint64_t)lane * VEC;
         if (piece >= a.npieces) {  // warp-uniform
             if constexpr (SYNC == 2) {
-                run_piece<VEC, NPT, POLICY, SYNC, IDLE>(a, base, 0, r);
+                run_piece<VEC, NPT, POLICY, SYNC, IDLE, OUT>(a, base, 0, r);
                 continue;
             } else {
                 break;
@@ -263,9 +285,9 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
         const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
         const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - first < wpb ? a.npieces - first : wpb);
         if ((piece + 1) * PIECE <= a.count)
-            run_piece<VEC, NPT, POLICY, SYNC, FULL>(a, base, bar_threads, r);
+            run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT>(a, base, bar_threads, r);
         else
-            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL>(a, base, bar_threads, r);
+            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL, OUT>(a, base, bar_threads, r);
     }
 }
 

@@ -2,7 +2,7 @@
  * rng_b200 -- NEXT-1: the paper's example program on the B200 path (§5).
  *
  *   rng_b200 n i [--seed S] [--mode O2|O1|O3|S0|S1] [--batch T] [--device D]
- *                [--profile] [--export FILE]
+ *                [--star] [--profile] [--export FILE]
  *
  * "a standalone program which outputs random numbers in binary format to the standard
  * output ... The program accepts two parameters: a) n, the quantity of 64-bit (8-byte)
@@ -28,7 +28,8 @@
 static void usage(FILE *f) {
     fprintf(f,
             "usage: rng_b200 n i [--seed S] [--mode O2|O1|O3|S0|S1] [--batch T] [--device D]\n"
-            "                [--profile] [--export FILE]\n"
+            "                [--star] [--profile] [--export FILE]\n"
+            "  --star  xorshift64*-scrambled output (state * 0x2545F4914F6CDD1D)\n"
             "  n  64-bit random values per iteration (1 .. 2^32)\n"
             "  i  iterations (>= 1); writes 8*n*i bytes to stdout\n");
 }
@@ -64,7 +65,7 @@ static int sink_stdout(void *user, uint64_t iter_begin, uint32_t iters, uint64_t
 
 int main(int argc, char **argv) {
     uint64_t n = 0, iters = 0, seed = 0, batch = 0;
-    int mode = PRNG_MODE_OVERLAP2, device = -1, profile = 0, npos = 0;
+    int mode = PRNG_MODE_OVERLAP2, device = -1, profile = 0, npos = 0, star = 0;
     const char *export_path = NULL;
     for (int a = 1; a < argc; ++a) {
         const char *s = argv[a];
@@ -85,6 +86,8 @@ int main(int argc, char **argv) {
             else if (!strcmp(m, "O2")) mode = PRNG_MODE_OVERLAP2;
             else if (!strcmp(m, "O3")) mode = PRNG_MODE_ZEROCOPY;
             else return usage(stderr), 2;
+        } else if (!strcmp(s, "--star")) {
+            star = 1;
         } else if (!strcmp(s, "--profile")) {
             profile = 1;
         } else if (!strcmp(s, "--export") && a + 1 < argc) {
@@ -112,6 +115,7 @@ int main(int argc, char **argv) {
     int rc = prng_set_option(h, PRNG_OPT_MODE, mode, &err);
     if (!rc) rc = prng_set_option(h, PRNG_OPT_BATCH_ITERS, (int64_t)batch, &err);
     if (!rc) rc = prng_set_option(h, PRNG_OPT_PROFILE, profile, &err);
+    if (!rc) rc = prng_set_option(h, PRNG_OPT_OUTPUT, star, &err);
     if (!rc) rc = prng_init(h, &err);
     if (!rc) rc = prng_generate(h, iters, sink_stdout, NULL, &err);
     if (rc) {

@@ -326,3 +326,47 @@ def test_host_memory_kinds(kind):
     finally:
         P.prng_destroy(h)
     assert np.array_equal(out, oracle.stream(n, i, 3))
+
+
+@pytest.mark.parametrize("kv", range(4))
+def test_star_output_all_paths(kv):
+    """NEXT-3 (A19): scrambled output through e2e (O2, O3) and device-only, vs the oracle."""
+    n, i = 4100, 7
+    want = oracle.stream_star(n, i, 6)
+    for mode in (P.PRNG_MODE_OVERLAP2, P.PRNG_MODE_ZEROCOPY):
+        h = P.prng_create(n, 6)
+        try:
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, kv)
+            P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
+            P.prng_set_option(h, P.PRNG_OPT_MODE, mode)
+            P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 3)
+            out = np.zeros((i, n), np.uint64)
+            P.prng_init(h)
+            P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0))
+            assert np.array_equal(out, want)
+            # the state stays the plain recurrence
+            assert np.array_equal(P.prng_read_state(h, n), oracle.stream(n, i, 6)[-1])
+        finally:
+            P.prng_destroy(h)
+    h = P.prng_create(n, 6)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, kv)
+        P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
+        P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, 8)
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        _, _, _, first, _ = P.prng_device_ring(h)
+        for k in range(i):
+            assert np.array_equal(P.prng_read_slot(h, (first + k) % 8, n), want[k])
+    finally:
+        P.prng_destroy(h)
+
+
+def test_star_output_rejects_other_variants():
+    h = P.prng_create(64, 0)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, 5)
+        with pytest.raises(P.PrngError):
+            P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
+    finally:
+        P.prng_destroy(h)

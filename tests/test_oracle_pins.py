@@ -299,3 +299,22 @@ def test_bounds_rejected():
         oracle.digest((1 << 32) + 1, 1, count=1)
     with pytest.raises(ValueError):
         oracle.stream(10, 1, gid_begin=8, count=3)
+
+
+# ---------------------------------------------------------------- NEXT-3: scrambled output
+def test_star_multiplier_is_vignas_and_invertible():
+    """A19: the scrambler multiplies by Vigna's xorshift64* constant M32 = 2685821657736338717
+    (odd, so a bijection); multiplying by its modular inverse recovers the pinned state."""
+    M = 2685821657736338717
+    assert M == 0x2545F4914F6CDD1D and M % 2 == 1
+    inv = pow(M, -1, 1 << 64)
+    r = np.random.default_rng(4)
+    for x in [0, 1, M64] + [int(v) for v in r.integers(0, 1 << 63, 200, dtype=np.uint64)]:
+        y = oracle.star(x)
+        assert (y * inv) & M64 == x
+        assert y & 1 == x & 1          # odd multiplier keeps the lowest bit
+    s = oracle.stream(777, 5, 8)
+    t = oracle.stream_star(777, 5, 8)
+    back = (t.astype(object) * inv) % (1 << 64)
+    assert np.array_equal(back.astype(np.uint64), s)
+    assert oracle.star(1) == M

@@ -1,0 +1,66 @@
+#!/usr/bin/env python3
+"""NEXT-4: the paper's Fig. 4 grid (n = 2^12, 2^14, ..., 2^24; i = 10^2, 10^3, 10^4;
+P:334-335) on the B200 path: device-only and end-to-end throughput per (n, i), plus the
+launch/host overhead visible at small n ("a larger n masks the ... overhead").
+
+    python tools/fig4_grid.py [--e2e-cap-gb 20] > fig4.jsonl
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1609_01257_b200 as P  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--e2e-cap-gb", type=float, default=20.0)
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    gen, cop = torch.cuda.Stream(), torch.cuda.Stream()
+    for lg in range(12, 25, 2):
+        n = 1 << lg
+        h = P.prng_create(n, 0)
+        P.prng_set_streams(h, gen.cuda_stream, cop.cuda_stream)
+        for it in (100, 1000, 10000):
+            nbytes = 8 * n * it
+            # device only: CUDA events around init + generate, best of 3 after a warm-up
+            P.prng_init(h)
+            P.prng_generate(h, it)
+            best = None
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                e0.record(gen)
+                P.prng_init(h)
+                P.prng_generate(h, it)
+                e1.record(gen)
+                torch.cuda.synchronize()
+                wall = time.perf_counter() - t0
+                ms = e0.elapsed_time(e1)
+                best = min(best or 1e30, ms)
+            row = {"n": f"2^{lg}", "i": it, "bytes": nbytes, "device_ms": best,
+                   "device_gbs": nbytes / (best * 1e-3) / 1e9, "device_numbers_per_s": n * it / (best * 1e-3),
+                   "host_wall_ms": wall * 1e3}
+            if nbytes <= a.e2e_cap_gb * 1e9:
+                P.prng_init(h)
+                P.prng_generate(h, min(it, 4), P.SINK_NULL)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                P.prng_init(h)
+                P.prng_generate(h, it, P.SINK_NULL)
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+                row.update({"e2e_ms": dt * 1e3, "e2e_gbs": nbytes / dt / 1e9})
+            print(json.dumps(row), flush=True)
+        P.prng_destroy(h)
+
+
+if __name__ == "__main__":
+    main()
