@@ -141,9 +141,12 @@ enum prng_option {
                                   1 write-combined, 2 THP-backed mmap + cudaHostRegister  */
     PRNG_OPT_TRACE_PTR = 9,    /* diagnostic: device pointer receiving %globaltimer stamps
                                   [CTA][round][iteration / 64] from variant "v2n4s1t"      */
-    PRNG_OPT_OUTPUT = 10       /* NEXT-3 output transform: 0 = the state (the paper, A7);
+    PRNG_OPT_OUTPUT = 10,      /* NEXT-3 output transform: 0 = the state (the paper, A7);
                                   1 = state * 0x2545F4914F6CDD1D mod 2^64 (xorshift64*-style
                                   scrambler, A19).  Needs kernel variant 0..3.              */
+    PRNG_OPT_TIME_PARALLEL = 11 /* 1 (default): when numrn is too small to fill the GPU, cut
+                                  a launch's iterations into chunks started by GF(2)
+                                  jump-ahead (xs^k is linear: a 64x64 bit matrix); 0: off */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two

@@ -119,7 +119,11 @@ struct prng {
     uint64_t pos = 0;  // iterations emitted since prng_init
     bool inited = false, poisoned = false;
 
-    uint64_t *d_state = nullptr;  // [round_up(count, 4)]
+    uint64_t *d_state = nullptr;   // [round_up(count, 4)]
+    uint64_t *d_state2 = nullptr;  // the other half of the state double buffer (time-parallel launches)
+    uint64_t *d_jump = nullptr;    // jump-ahead columns [chunks][64] (time-parallel launches)
+    uint64_t jump_cap = 0, jump_key[3] = {0, 0, 0};  // capacity (chunks), cached (C, L, e)
+    int time_parallel = 1;         // PRNG_OPT_TIME_PARALLEL
 
     // device-only ring
     uint64_t *d_ring = nullptr;
@@ -253,6 +257,10 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     a.iters = iters;
     a.first_is_state = first_is_state ? 1u : 0u;
     a.trace = h->trace;
+    a.nchunks = 1;
+    a.chunk_len = iters;
+    a.jump = nullptr;
+    a.state_out = h->d_state;
 
     const uint64_t piece = 32ull * v.npt;
     a.npieces = (h->count + piece - 1) / piece;
@@ -263,8 +271,41 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     else if (v.warps_per_sm > 0)
         max_warps = std::min<uint64_t>(max_warps, (uint64_t)v.warps_per_sm * h->num_sms);
     max_warps = std::max<uint64_t>(max_warps, kBlock / 32);
-    const uint64_t rounds0 = (a.npieces + max_warps - 1) / max_warps;
-    uint64_t warps = (a.npieces + rounds0 - 1) / rounds0;
+    // Time-parallel mode (NEXT-4): when the pieces cannot fill the grid (small numrn), cut
+    // the launch's iterations into chunks started by GF(2) jump-ahead, so that
+    // pieces x chunks units fill it.
+    uint64_t units = a.npieces;
+    // (chunks >= 256 iterations keep the per-unit 64-step mat-vec below ~10 % of its work)
+    if (h->time_parallel && v.stages == 0 && 2 * a.npieces <= max_warps && iters >= 512) {
+        uint64_t C = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
+        if (C > 1) {
+            const uint64_t L = (iters + C - 1) / C;
+            C = (iters + L - 1) / L;
+            if (C > h->jump_cap) {
+                if (h->d_jump) cudaFree(h->d_jump);
+                h->d_jump = nullptr;
+                h->jump_cap = 0;
+                CU(cudaMalloc(&h->d_jump, C * 64 * sizeof(uint64_t)));
+                h->jump_cap = C;
+                h->jump_key[0] = 0;
+            }
+            const uint64_t e = first_is_state ? 0 : 1;
+            if (h->jump_key[0] != C || h->jump_key[1] != L || h->jump_key[2] != e) {
+                prngk::jump_columns_kernel<<<1, 64, 0, s>>>(h->d_jump, (uint32_t)C, (uint32_t)L, (uint32_t)e);
+                CU(cudaGetLastError());
+                h->jump_key[0] = C;
+                h->jump_key[1] = L;
+                h->jump_key[2] = e;
+            }
+            a.nchunks = (uint32_t)C;
+            a.chunk_len = (uint32_t)L;
+            a.jump = h->d_jump;
+            a.state_out = h->d_state2;  // chunks read d_state; the last chunk writes the other half
+            units = a.npieces * C;
+        }
+    }
+    const uint64_t rounds0 = (units + max_warps - 1) / max_warps;
+    uint64_t warps = (units + rounds0 - 1) / rounds0;
     // Spread the warps over all SMs: with <= 8 warps per SM use one CTA per SM of
     // ceil(warps / SMs) warps, else 256-thread CTAs.
     uint64_t wpb = kBlock / 32;
@@ -287,7 +328,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
         if (max_cl < 1) return set_err(err, PRNG_ECUDA, "cluster of %llu CTAs cannot be resident", (unsigned long long)C);
         blocks = std::min<uint64_t>((blocks + C - 1) / C, (uint64_t)max_cl) * C;
     }
-    a.rounds = (uint32_t)((a.npieces + blocks * wpb - 1) / (blocks * wpb));
+    a.rounds = (uint32_t)((units + blocks * wpb - 1) / (blocks * wpb));
     if (int rc = prof_begin(h, s, PRNG_EV_RNG_KERNEL, err)) return rc;
     if (C > 1) {
         cudaLaunchConfig_t cfg = {};
@@ -304,6 +345,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     } else {
         v.fn<<<(unsigned)blocks, (unsigned)(32 * wpb), variant_smem(v, wpb), s>>>(a);
     }
+    if (a.nchunks > 1) std::swap(h->d_state, h->d_state2);  // the final state is in the other half
     CU(cudaGetLastError());
     return prof_end(h, s, err);
 }
@@ -402,6 +444,8 @@ prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begi
     }
     if ((e = cudaMalloc(&h->d_state, pitch_for(gid_count) * sizeof(uint64_t))) != cudaSuccess)
         return bail("cudaMalloc(state)", e);
+    if ((e = cudaMalloc(&h->d_state2, pitch_for(gid_count) * sizeof(uint64_t))) != cudaSuccess)
+        return bail("cudaMalloc(state2)", e);
     if ((e = cudaStreamCreateWithFlags(&h->s_gen, cudaStreamNonBlocking)) != cudaSuccess)
         return bail("cudaStreamCreate", e);
     if ((e = cudaStreamCreateWithFlags(&h->s_copy, cudaStreamNonBlocking)) != cudaSuccess)
@@ -423,6 +467,8 @@ void prng_destroy(prng_t *h) {
     free_e2e(h);
     if (h->d_ring) cudaFree(h->d_ring);
     if (h->d_state) cudaFree(h->d_state);
+    if (h->d_state2) cudaFree(h->d_state2);
+    if (h->d_jump) cudaFree(h->d_jump);
     if (h->own_streams) {
         if (h->s_gen) cudaStreamDestroy(h->s_gen);
         if (h->s_copy) cudaStreamDestroy(h->s_copy);
@@ -480,6 +526,9 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
                 return set_err(err, PRNG_EINVAL, "output scrambling needs kernel variant < %d", kNumStar);
             h->kernel = (int)value;
             break;
+        case PRNG_OPT_TIME_PARALLEL:
+            h->time_parallel = value ? 1 : 0;
+            break;
         case PRNG_OPT_OUTPUT:
             if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad output transform");
             if (value == 1 && h->kernel >= kNumStar)
@@ -518,6 +567,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_PROFILE: *value = h->profile; break;
         case PRNG_OPT_KERNEL: *value = h->kernel; break;
         case PRNG_OPT_OUTPUT: *value = h->output; break;
+        case PRNG_OPT_TIME_PARALLEL: *value = h->time_parallel; break;
         case PRNG_OPT_GRID_WARPS: *value = h->grid_warps; break;
         case PRNG_OPT_RING_PAD: *value = h->ring_pad; break;
         case PRNG_OPT_HOST_MEM: *value = h->host_mem; break;
@@ -756,10 +806,10 @@ static int ensure_e2e(prng *h, uint64_t T, int halves, int kind, bool need_dbuf,
 // O3 (zero-copy): the generation kernel stores each batch straight into a mapped pinned
 // host half over PCIe -- no device ring, no copy engine; the store IS the transfer.
 // sink(j) runs while gen(j+1) writes the other half; gen(j+2) is enqueued after sink(j).
-static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, prng_sink_fn sink, void *user,
-                             prng_err_t *err) {
+static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, uint64_t T_alloc, prng_sink_fn sink,
+                             void *user, prng_err_t *err) {
     if (h->count % 4) return set_err(err, PRNG_EINVAL, "zero-copy mode needs count %% 4 == 0 (32-B aligned rows)");
-    if (int rc = ensure_e2e(h, T, 2, HK_MAPPED, false, err)) return rc;
+    if (int rc = ensure_e2e(h, T_alloc, 2, HK_MAPPED, false, err)) return rc;
     const double t0 = now_s();  // wall time of the profiled call, allocations excluded
     const uint64_t nb = (numiter + T - 1) / T;
     const uint64_t pos0 = h->pos;
@@ -816,13 +866,14 @@ static int generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void *user
     uint64_t T = (uint64_t)h->batch_iters;
     const uint64_t row = h->count * sizeof(uint64_t);
     if (T == 0) T = std::max<uint64_t>(1, (256ull << 20) / row);  // ~256 MiB per batch
+    const uint64_t T_alloc = T;  // buffers are sized for full batches: no re-allocation per call
     T = std::min<uint64_t>(T, numiter);
     const int mode = h->mode;
     if (mode == PRNG_MODE_ZEROCOPY) {
-        return generate_zerocopy(h, numiter, T, sink, user, err);
+        return generate_zerocopy(h, numiter, T, T_alloc, sink, user, err);
     }
     const int halves = (mode == PRNG_MODE_OVERLAP2 || mode == PRNG_MODE_PAGEABLE) ? 2 : 1;
-    if (int rc = ensure_e2e(h, T, halves, mode == PRNG_MODE_PAGEABLE ? HK_PAGEABLE : h->host_mem, true, err))
+    if (int rc = ensure_e2e(h, T_alloc, halves, mode == PRNG_MODE_PAGEABLE ? HK_PAGEABLE : h->host_mem, true, err))
         return rc;
     const uint64_t nb = (numiter + T - 1) / T;
     const uint64_t pitch = h->buf_pitch;

@@ -150,8 +150,73 @@ struct BatchArgs {
     uint32_t first_is_state;  // 1: the launch's first iteration is iteration 0 (= the seeds):
                               //    emit the state unchanged, then step (A6)
     uint64_t npieces;         // ceil(count / (32 * NPT))
-    uint32_t rounds;          // ceil(npieces / warps in grid)
+    uint32_t rounds;          // ceil(npieces * nchunks / warps in grid)
     unsigned long long *trace;  // SYNC 3 (diagnostic): %globaltimer per CTA, round, 64 iterations
+    // Time-parallel mode (NEXT-4, small numrn): the launch's iterations are cut into nchunks
+    // chunks of chunk_len; chunk c starts from J_c * state where J_c = T^(c*chunk_len + e)
+    // is the GF(2) matrix of xs^(c*chunk_len + e) (e = 0 if first_is_state else 1), stored
+    // as 64 columns J_c e_i at jump[c*64 + i].  nchunks == 1: the plain sequential mode.
+    uint32_t nchunks;
+    uint32_t chunk_len;
+    const uint64_t *jump;     // [nchunks][64] (nchunks > 1)
+    uint64_t *state_out;      // nchunks > 1: the last chunk writes the final state here
+};
+
+// y = J x over GF(2): XOR of the columns J e_i selected by the bits of x (xs^k is linear).
+__device__ __forceinline__ uint64_t gf2_matvec(const uint64_t *__restrict__ J, uint64_t x) {
+    uint64_t y = 0;
+#pragma unroll 16
+    for (int i = 0; i < 64; ++i) y ^= __ldg(J + i) & (0ull - ((x >> i) & 1ull));
+    return y;
+}
+
+// Columns of J_c = T^(c*L + e), c = 0..C-1, by one CTA of 64 threads (thread i owns column
+// i; xs is GF(2)-linear, so the column T^k e_i is xs^k(e_i)).  P = T^L by binary
+// exponentiation (log2 L matrix products, each column a 64-step mat-vec against the other
+// matrix's columns in shared memory), J_0 = T^e, J_c = P * J_{c-1}.
+__device__ __forceinline__ uint64_t gf2_matvec_smem(const uint64_t *M, uint64_t x) {
+    uint64_t y = 0;
+#pragma unroll 16
+    for (int b = 0; b < 64; ++b) y ^= M[b] & (0ull - ((x >> b) & 1ull));
+    return y;
+}
+
+__global__ void __launch_bounds__(64) jump_columns_kernel(uint64_t *jump, uint32_t C, uint32_t L, uint32_t e) {
+    __shared__ uint64_t B[64], R[64];
+    const uint32_t i = threadIdx.x;
+    const uint64_t t_col = xorshift64(1ull << i);  // T e_i
+    B[i] = t_col;
+    R[i] = 1ull << i;  // identity
+    __syncthreads();
+    for (uint32_t k = L; k; k >>= 1) {
+        if (k & 1) {
+            const uint64_t r = gf2_matvec_smem(B, R[i]);  // R = B R
+            __syncthreads();
+            R[i] = r;
+            __syncthreads();
+        }
+        const uint64_t b = gf2_matvec_smem(B, B[i]);  // B = B B
+        __syncthreads();
+        B[i] = b;
+        __syncthreads();
+    }
+    // R = P = T^L (column i in R[i])
+    uint64_t col = e ? t_col : (1ull << i);
+    jump[i] = col;
+    for (uint32_t c = 1; c < C; ++c) {
+        col = gf2_matvec_smem(R, col);
+        jump[(uint64_t)c * 64 + i] = col;
+    }
+}
+
+// One work unit of a warp: the gids of one piece over iterations [t_begin, t_begin + t_count).
+struct Unit {
+    uint64_t base;         // this lane's first gid (handle-relative) of the piece
+    uint32_t t_begin;      // first iteration of the launch this unit emits
+    uint32_t t_count;      // iterations it emits
+    const uint64_t *jump;  // nullptr: start from the state; else from J * state
+    uint64_t *state_out;   // nullptr: do not write the state back
+    bool emit_first;       // true: the unit's first iteration emits its start value unchanged
 };
 
 // Warp coherence (SYNC):
@@ -174,11 +239,12 @@ __device__ __forceinline__ void cluster_arrive() {
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
 template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0>
-__device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uint32_t bar_threads,
+__device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uint32_t bar_threads,
                                           uint32_t trace_round) {
     constexpr int NV = NPT / VEC;
+    const uint64_t base = u.base;
     uint64_t x[NPT];
-    // ---- load the NPT states of this lane (read once per launch)
+    // ---- load the NPT states of this lane (read once per unit)
     if constexpr (MODE == FULL) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
@@ -194,42 +260,49 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uin
 #pragma unroll
         for (int j = 0; j < NPT; ++j) x[j] = 0;
     }
-    uint64_t *p = a.dst + (uint64_t)a.slot0 * a.pitch + base;
-    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
-    uint32_t slot = a.slot0;
-    for (uint32_t t = 0; t < a.iters; ++t) {
-        if constexpr (MODE != IDLE) {
-            if (t > 0 || !a.first_is_state) {
+    if constexpr (MODE != IDLE) {
+        if (u.jump) {  // time-parallel chunk: jump ahead (c*L + e) steps in one GF(2) mat-vec
 #pragma unroll
-                for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
-            }
+            for (int j = 0; j < NPT; ++j) x[j] = gf2_matvec(u.jump, x[j]);
         }
+    }
+    uint32_t slot = (uint32_t)(((uint64_t)a.slot0 + u.t_begin) % a.nslots);
+    uint64_t *p = a.dst + (uint64_t)slot * a.pitch + base;
+    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
+    // One loop trip: store this iteration (if the unit is active), meet the CTA / cluster
+    // barrier, advance to the next ring slot.  Every unit of a launch makes the same number
+    // of trips (the barriers of SYNC 1 / 2 must match): a shorter last chunk idles through
+    // its surplus trips.  The first trip is peeled so the hot loop has no conditions.
+    auto trip = [&](uint32_t t, bool active) {
         if constexpr (SYNC == 2) {
             if (t > 0) cluster_wait();
         }
-        if constexpr (MODE == FULL) {
+        if (active) {
+            if constexpr (MODE == FULL) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                if constexpr (OUT == 0) {
-                    store_vec<VEC, POLICY>(p + v * 32 * VEC, x + v * VEC);
-                } else {
-                    uint64_t y[VEC];
+                for (int v = 0; v < NV; ++v) {
+                    if constexpr (OUT == 0) {
+                        store_vec<VEC, POLICY>(p + v * 32 * VEC, x + v * VEC);
+                    } else {
+                        uint64_t y[VEC];
 #pragma unroll
-                    for (int e = 0; e < VEC; ++e) y[e] = emit<OUT>(x[v * VEC + e]);
-                    store_vec<VEC, POLICY>(p + v * 32 * VEC, y);
+                        for (int e = 0; e < VEC; ++e) y[e] = emit<OUT>(x[v * VEC + e]);
+                        store_vec<VEC, POLICY>(p + v * 32 * VEC, y);
+                    }
                 }
+            } else if constexpr (MODE == PARTIAL) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e)
+                        if (base + (uint64_t)v * 32 * VEC + e < a.count)
+                            p[v * 32 * VEC + e] = emit<OUT>(x[v * VEC + e]);
             }
-        } else if constexpr (MODE == PARTIAL) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v)
-#pragma unroll
-                for (int e = 0; e < VEC; ++e)
-                    if (base + (uint64_t)v * 32 * VEC + e < a.count) p[v * 32 * VEC + e] = emit<OUT>(x[v * VEC + e]);
         }
         if constexpr (SYNC == 1 || SYNC == 3) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
         if constexpr (SYNC == 3) {
             // drift diagnostic: CTA-leader timestamps every 64 iterations
-            if ((t & 63) == 0 && (threadIdx.x & 31) == 0 && bar_threads > 0 && a.trace && threadIdx.x == 0) {
+            if ((t & 63) == 0 && bar_threads > 0 && a.trace && threadIdx.x == 0) {
                 unsigned long long ts;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
                 const uint64_t per_round = (a.iters + 63) / 64;
@@ -237,28 +310,72 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, uint64_t base, uin
             }
         }
         if constexpr (SYNC == 2) cluster_arrive();
-        // advance to the next slot of the ring (warp-uniform)
-        if (++slot == a.nslots) {
+        if (++slot == a.nslots) {  // warp-uniform
             slot = 0;
             p -= wrap;
         } else {
             p += a.pitch;
         }
+    };
+    auto step = [&]() {
+        if constexpr (MODE != IDLE) {
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
+        }
+    };
+    const uint32_t t_loop = a.nchunks > 1 ? a.chunk_len : a.iters;
+    const uint32_t t_act = MODE == IDLE ? 0u : u.t_count;
+    uint32_t t = 0;
+    if (t_act > 0) {
+        if (!u.emit_first) step();
+        trip(0, true);
+        t = 1;
     }
+    for (; t < t_act; ++t) {  // the hot loop
+        step();
+        trip(t, true);
+    }
+    for (; t < t_loop; ++t) trip(t, false);  // idle trips (short last chunk, IDLE units)
     if constexpr (SYNC == 2) cluster_wait();  // balance the last arrive
-    // ---- write the state back (== the launch's last iteration)
-    if constexpr (MODE == FULL) {
+    // ---- write the state back (== the unit's last iteration) if this unit ends the launch
+    if (u.state_out) {
+        if constexpr (MODE == FULL) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
-    } else if constexpr (MODE == PARTIAL) {
+            for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(u.state_out + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+        } else if constexpr (MODE == PARTIAL) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
+            for (int v = 0; v < NV; ++v)
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                const uint64_t idx = base + (uint64_t)v * 32 * VEC + e;
-                if (idx < a.count) a.state[idx] = x[v * VEC + e];
-            }
+                for (int e = 0; e < VEC; ++e) {
+                    const uint64_t idx = base + (uint64_t)v * 32 * VEC + e;
+                    if (idx < a.count) u.state_out[idx] = x[v * VEC + e];
+                }
+        }
     }
+}
+
+// The work unit dealt to a warp: unit index w -> (piece = w mod npieces, chunk = w div
+// npieces), so adjacent warps hold adjacent pieces of the same chunk.
+template <int NPT, int VEC>
+__device__ __forceinline__ Unit make_unit(const BatchArgs &a, uint64_t unit, uint32_t lane) {
+    Unit u;
+    const uint64_t piece = unit % a.npieces, chunk = unit / a.npieces;
+    u.base = piece * 32ull * NPT + (uint64_t)lane * VEC;
+    if (a.nchunks <= 1) {
+        u.t_begin = 0;
+        u.t_count = a.iters;
+        u.jump = nullptr;
+        u.state_out = a.state;  // in place: each lane reads then writes its own states
+        u.emit_first = a.first_is_state != 0;
+    } else {
+        u.t_begin = (uint32_t)chunk * a.chunk_len;
+        const uint32_t left = a.iters - u.t_begin;
+        u.t_count = left < a.chunk_len ? left : a.chunk_len;
+        u.jump = a.jump + chunk * 64;
+        u.state_out = (chunk + 1 == a.nchunks) ? a.state_out : nullptr;
+        u.emit_first = true;
+    }
+    return u;
 }
 
 template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0>
@@ -270,24 +387,29 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t cta_warp0 = (uint64_t)blockIdx.x * wpb;
+    const uint64_t nunits = a.npieces * (a.nchunks ? a.nchunks : 1);
     for (uint32_t r = 0; r < a.rounds; ++r) {
-        const uint64_t piece = (uint64_t)r * nwarps + warp;
-        const uint64_t base = piece * PIECE + (uint64_t)lane * VEC;
-        if (piece >= a.npieces) {  // warp-uniform
+        const uint64_t unit = (uint64_t)r * nwarps + warp;
+        if (unit >= nunits) {  // warp-uniform
             if constexpr (SYNC == 2) {
-                run_piece<VEC, NPT, POLICY, SYNC, IDLE, OUT>(a, base, 0, r);
+                Unit u = make_unit<NPT, VEC>(a, 0, lane);
+                u.state_out = nullptr;
+                u.t_count = a.nchunks <= 1 ? a.iters : a.chunk_len;
+                run_piece<VEC, NPT, POLICY, SYNC, IDLE, OUT>(a, u, 0, r);
                 continue;
             } else {
                 break;
             }
         }
-        // warps of this CTA holding a piece in round r: a prefix of the CTA's warps
+        const Unit u = make_unit<NPT, VEC>(a, unit, lane);
+        // warps of this CTA holding a unit in round r: a prefix of the CTA's warps
         const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
-        const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - first < wpb ? a.npieces - first : wpb);
+        const uint32_t bar_threads = 32u * (uint32_t)(nunits - first < wpb ? nunits - first : wpb);
+        const uint64_t piece = unit % a.npieces;
         if ((piece + 1) * PIECE <= a.count)
-            run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT>(a, base, bar_threads, r);
+            run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT>(a, u, bar_threads, r);
         else
-            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL, OUT>(a, base, bar_threads, r);
+            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL, OUT>(a, u, bar_threads, r);
     }
 }
 
@@ -357,7 +479,7 @@ __global__ void __launch_bounds__(256) batch_kernel_tma(BatchArgs a) {
         if ((piece + 1) * PIECE <= a.count)
             run_piece_tma<NPT, STAGES>(a, piece, lane, wbuf);
         else
-            run_piece<2, NPT, 0, 0, PARTIAL>(a, piece * PIECE + 2ull * lane, 0, r);
+            run_piece<2, NPT, 0, 0, PARTIAL>(a, make_unit<NPT, 2>(a, piece, lane), 0, r);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }

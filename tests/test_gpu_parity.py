@@ -370,3 +370,65 @@ def test_star_output_rejects_other_variants():
             P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
     finally:
         P.prng_destroy(h)
+
+
+# ---------------------------------------------------------------- NEXT-4: time-parallel jump-ahead
+@pytest.mark.parametrize("n", [1, 33, 1000, 4099])
+@pytest.mark.parametrize("i", [300, 1001, 2600])
+def test_time_parallel_device_only(n, i):
+    """Small numrn: the launch is cut into iteration chunks started by GF(2) jump-ahead.
+    Every output of every iteration vs the oracle, and the final state."""
+    import torch
+    pitch = (n + 3) // 4 * 4
+    buf = torch.zeros((i, pitch), dtype=torch.int64, device="cuda")
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_init(h)
+        P.prng_generate_device(h, i, buf.data_ptr(), pitch, i, 0)
+        torch.cuda.synchronize()
+        want = oracle.stream(n, i, SEED_PARITY)
+        assert np.array_equal(buf[:, :n].cpu().numpy().view(np.uint64), want)
+        assert np.array_equal(P.prng_read_state(h, n), want[-1])
+    finally:
+        P.prng_destroy(h)
+
+
+@pytest.mark.parametrize("batch", [0, 700, 1])
+@pytest.mark.parametrize("kv", [0, 1, 4, 12])
+def test_time_parallel_e2e_and_split(batch, kv):
+    """Chunked batches (alternating e = 0 / 1 jump offsets), split calls, several variants."""
+    n, i = 1000, 3000
+    want = oracle.stream(n, i, 17)
+    got = run_e2e(n, i, 17, batch=batch, kernel=kv, calls=[1000, 1313, 687])
+    assert np.array_equal(got, want)
+
+
+def test_time_parallel_off_is_identical():
+    n, i = 777, 1400
+    outs = []
+    for tp in (0, 1):
+        h = P.prng_create(n, 5)
+        try:
+            P.prng_set_option(h, P.PRNG_OPT_TIME_PARALLEL, tp)
+            out = np.zeros((i, n), np.uint64)
+            P.prng_init(h)
+            P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0))
+            outs.append(out)
+        finally:
+            P.prng_destroy(h)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], oracle.stream(n, i, 5))
+
+
+@pytest.mark.parametrize("kv", range(4))
+def test_time_parallel_star(kv):
+    n, i = 512, 1333
+    h = P.prng_create(n, 2)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, kv)
+        P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
+        out = np.zeros((i, n), np.uint64)
+        P.prng_init(h)
+        P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0))
+    finally:
+        P.prng_destroy(h)
+    assert np.array_equal(out, oracle.stream_star(n, i, 2))
