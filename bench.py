@@ -385,6 +385,11 @@ def run_ours(a, D):
 
 def main():
     a = parse()
+    if a.impl != "reference" and a.dist_backend == "nccl":
+        # bind this rank's GPU before the process group exists (NCCL uses the current device)
+        import torch
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local % a.device_mod if a.device_mod > 0 else local)
     D = Dist(None if a.impl == "reference" else a.dist_backend)
     try:
         if a.impl == "reference":
