@@ -264,9 +264,12 @@ def run_ours(a, D):
     for _ in range(a.warmup):
         P.prng_init(h)
         P.prng_generate(h, a.numiter)
-    P.prng_set_option(h, P.PRNG_OPT_PROFILE, 1)
+    # Timed region: K steps enqueued back to back on the generation stream (no host round
+    # trips between steps: PRNG_OPT_BLOCKING 0), per-launch CUDA-event intervals accumulated
+    # (PRNG_OPT_PROFILE 2) and read after the region.
+    P.prng_set_option(h, P.PRNG_OPT_PROFILE, 2)
+    P.prng_set_option(h, P.PRNG_OPT_BLOCKING, 0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kern_ms, init_ms, launches = [], [], 0
     with Clocks(dev) as clk:
         D.barrier()
         torch.cuda.synchronize()
@@ -274,13 +277,14 @@ def run_ours(a, D):
         for _ in range(a.steps):
             P.prng_init(h)
             P.prng_generate(h, a.numiter)
-            ids, s, e, _ = P.prng_prof_events(h)  # per-launch CUDA-event intervals of this step
-            kern_ms += [1e3 * (y - x) for i, x, y in zip(ids, s, e) if i == 1]
-            init_ms += [1e3 * (y - x) for i, x, y in zip(ids, s, e) if i == 0]
-            launches += len(ids)
         ev1.record(gen)
         torch.cuda.synchronize()
         D.barrier()
+    P.prng_set_option(h, P.PRNG_OPT_BLOCKING, 1)
+    ids, s, e, _ = P.prng_prof_events(h)  # per-launch CUDA-event intervals of the K steps
+    kern_ms = [1e3 * (y - x) for i, x, y in zip(ids, s, e) if i == 1]
+    init_ms = [1e3 * (y - x) for i, x, y in zip(ids, s, e) if i == 0]
+    launches = len(ids)
     ms = ev0.elapsed_time(ev1)
     P.prng_set_option(h, P.PRNG_OPT_PROFILE, 0)
     ms_max = D.max(ms)

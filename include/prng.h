@@ -132,7 +132,9 @@ enum prng_option {
     PRNG_OPT_MODE = 1,         /* enum prng_mode, default PRNG_MODE_OVERLAP2            */
     PRNG_OPT_BATCH_ITERS = 2,  /* T for end-to-end batches; 0 = auto (~256 MiB per batch) */
     PRNG_OPT_RING_SLOTS = 3,   /* R of the device-only ring; 0 = auto (64 GiB, <= 40 % free) */
-    PRNG_OPT_PROFILE = 4,      /* 1 = record per-batch intervals (CUDA events)           */
+    PRNG_OPT_PROFILE = 4,      /* 1 = record per-batch intervals (CUDA events), reset by
+                                  prng_init; 2 = same, accumulated across prng_init calls
+                                  and without the host syncs mode 1 adds for wall time    */
     PRNG_OPT_KERNEL = 5,       /* kernel variant id (see prng_kernel_variants); 0 = default */
     PRNG_OPT_GRID_WARPS = 6,   /* cap on resident warps of the persistent grid; 0 = auto  */
     PRNG_OPT_RING_PAD = 7,     /* extra u64 elements between device-only ring slots (multiple
@@ -144,9 +146,12 @@ enum prng_option {
     PRNG_OPT_OUTPUT = 10,      /* NEXT-3 output transform: 0 = the state (the paper, A7);
                                   1 = state * 0x2545F4914F6CDD1D mod 2^64 (xorshift64*-style
                                   scrambler, A19).  Needs kernel variant 0..3.              */
-    PRNG_OPT_TIME_PARALLEL = 11 /* 1 (default): when numrn is too small to fill the GPU, cut
+    PRNG_OPT_TIME_PARALLEL = 11, /* 1 (default): when numrn is too small to fill the GPU, cut
                                   a launch's iterations into chunks started by GF(2)
                                   jump-ahead (xs^k is linear: a 64x64 bit matrix); 0: off */
+    PRNG_OPT_BLOCKING = 12     /* 1 (default): device-only prng_generate returns when the work
+                                  is done; 0: returns after enqueueing on the generation
+                                  stream (synchronise the stream before reading results)   */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two

@@ -149,7 +149,7 @@ struct prng {
     int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0, ring_pad = 0;
     unsigned long long *trace = nullptr;  // PRNG_OPT_TRACE_PTR (diagnostic variant only)
 
-    int profile = 0, kernel = 0, output = 0;
+    int profile = 0, kernel = 0, output = 0, blocking = 1;
     int blocks_per_sm[kNumVariants] = {0};
 
     // profiling (a6)
@@ -518,7 +518,17 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             h->ring_slots_opt = value;
             break;
         case PRNG_OPT_PROFILE:
-            h->profile = value ? 1 : 0;
+            if (value < 0 || value > 2) return set_err(err, PRNG_EINVAL, "bad profile mode");
+            if (value != h->profile) {
+                cudaSetDevice(h->device);
+                cudaStreamSynchronize(h->s_gen);
+                cudaStreamSynchronize(h->s_copy);
+                clear_prof(h);
+            }
+            h->profile = (int)value;
+            break;
+        case PRNG_OPT_BLOCKING:
+            h->blocking = value ? 1 : 0;
             break;
         case PRNG_OPT_KERNEL:
             if (value < 0 || value >= kNumVariants) return set_err(err, PRNG_EINVAL, "bad kernel variant");
@@ -565,6 +575,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_BATCH_ITERS: *value = h->batch_iters; break;
         case PRNG_OPT_RING_SLOTS: *value = h->ring_slots_opt; break;
         case PRNG_OPT_PROFILE: *value = h->profile; break;
+        case PRNG_OPT_BLOCKING: *value = h->blocking; break;
         case PRNG_OPT_KERNEL: *value = h->kernel; break;
         case PRNG_OPT_OUTPUT: *value = h->output; break;
         case PRNG_OPT_TIME_PARALLEL: *value = h->time_parallel; break;
@@ -584,7 +595,7 @@ int prng_init(prng_t *h, prng_err_t *err) {
     if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
     CU(cudaSetDevice(h->device));
     h->poisoned = false;
-    clear_prof(h);
+    if (h->profile != 2) clear_prof(h);  // 2: intervals accumulate across runs
     if (int rc = ensure_origin(h, err)) return rc;
     const double t0 = now_s();
     prngk::SeedArgs a{h->d_state, h->count, h->gid_begin, h->seed};
@@ -598,7 +609,7 @@ int prng_init(prng_t *h, prng_err_t *err) {
     h->pos = 0;
     h->ring_iter0 = h->ring_cursor;
     h->inited = true;
-    if (h->profile) {
+    if (h->profile == 1) {
         CU(cudaStreamSynchronize(h->s_gen));
         h->wall_s += now_s() - t0;
     }
@@ -679,8 +690,10 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
         done += it;
     }
     h->ring_cursor = (h->ring_iter0 + h->pos) % h->ring_slots;
-    CU(cudaStreamSynchronize(h->s_gen));
-    h->wall_s += now_s() - t0;
+    if (h->blocking) {
+        CU(cudaStreamSynchronize(h->s_gen));
+        h->wall_s += now_s() - t0;
+    }
     return PRNG_OK;
 }
 

@@ -432,3 +432,24 @@ def test_time_parallel_star(kv):
     finally:
         P.prng_destroy(h)
     assert np.array_equal(out, oracle.stream_star(n, i, 2))
+
+
+def test_nonblocking_accumulated_profile():
+    """bench.py's timed loop: PRNG_OPT_BLOCKING 0 + PRNG_OPT_PROFILE 2 -- K runs enqueued
+    back to back, intervals accumulated, results identical."""
+    import torch
+    n, i, K = 5000, 40, 3
+    h = P.prng_create(n, 8)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_PROFILE, 2)
+        P.prng_set_option(h, P.PRNG_OPT_BLOCKING, 0)
+        for _ in range(K):
+            P.prng_init(h)
+            P.prng_generate(h, i)
+        torch.cuda.synchronize()
+        ids, s, e, _ = P.prng_prof_events(h)
+        assert (ids == 0).sum() == K and (ids == 1).sum() == K and (e >= s).all()
+        P.prng_set_option(h, P.PRNG_OPT_BLOCKING, 1)
+        assert np.array_equal(P.prng_read_state(h, n), oracle.stream(n, i, 8)[-1])
+    finally:
+        P.prng_destroy(h)
