@@ -6,7 +6,7 @@
 
 One "step" = one pass of the whole hot path over one synthetic workload:
 prng_init (a1, seeding kernel) + prng_generate(numiter) (a2+a3: xorshift64 batch kernel,
-register-resident state, 32-byte stores into a device ring).  BASELINE.json's metric is
+register-resident state, 16-byte stores into a device ring).  BASELINE.json's metric is
 random numbers/s (and GB/s, 8 B per number, Eq. 1) device-only and end to end.
 
 * value      device-only numbers/s over all ranks: inputs (numrn, numiter, seed) resident,
