@@ -84,6 +84,9 @@ const Variant kVariants[] = {
     V("v4n8cs", 4, 8, 1, 0, 1, 0),    V("v2n8cs", 2, 8, 1, 0, 1, 0),
     // cluster barrier (split arrive / wait) every iteration (c2 ~ s1; c4 ~ 4.4 TB/s)
     V("v2n8c2", 2, 8, 0, 2, 2, 4),    V("v2n8c4", 2, 8, 0, 2, 4, 4),
+    // long per-CTA chunks: 32 / 64 numbers per thread (16 / 32 KiB per warp per iteration)
+    // (measured: no gain over v2n4s1; 64 numbers/thread spills and was removed)
+    V("v2n32s1", 2, 32, 0, 1, 1, 4),  V("v4n32s1", 4, 32, 0, 1, 1, 4),
     // diagnostic: v2n4s1 + per-CTA %globaltimer trace (PRNG_OPT_TRACE_PTR)
     V("v2n4s1t", 2, 4, 0, 3, 1, 4),
     // TMA bulk stores: one cp.async.bulk per warp per iteration from an smem stage ring

@@ -2,8 +2,9 @@
 //
 //   a1  seed_kernel   : state[g] = seed64(gid_begin + g, seed)          (readings A1-A4)
 //   a2+a3 batch_kernel: T iterations of xorshift64 per launch, state held in registers,
-//                       every iteration stored with 32-byte (or 16-byte) coalesced vector
+//                       every iteration stored with 16-byte (or 32-byte) coalesced vector
 //                       stores into a ring of iteration slots            (A5-A8)
+//   NEXT-4 jump_columns_kernel: GF(2) jump-ahead matrices for time-parallel launches
 //
 // The paper's OpenCL `prng` kernel re-reads its state from one buffer and writes the
 // successor to another every iteration (16 B/number of global traffic).
@@ -16,8 +17,10 @@
 //   lane l holds, for v in 0..NPT/VEC-1, the VEC consecutive gids at
 //   p*32*NPT + v*32*VEC + l*VEC  -> one warp-wide store instruction writes 32*VEC*8
 //   contiguous bytes (512 B for VEC = 2, 1 KiB for VEC = 4).
-//   warp w of W processes pieces w, w+W, w+2W, ... (`rounds` of them); the host sizes W so
-//   that every warp gets the same number of pieces +- 1 and the grid is <= one wave.
+//   warp w of W processes units w, w+W, w+2W, ... (`rounds` of them); a unit is a piece
+//   over all of the launch's iterations, or (time-parallel mode, small numrn) a piece
+//   over one chunk of them.  The host sizes W so that every warp gets the same number of
+//   units +- 1 and the grid is <= one wave.
 //
 // No code here is shared with oracle/ (the CPU definition); see DESIGN.md §2.
 #pragma once
