@@ -453,3 +453,67 @@ def test_nonblocking_accumulated_profile():
         assert np.array_equal(P.prng_read_state(h, n), oracle.stream(n, i, 8)[-1])
     finally:
         P.prng_destroy(h)
+
+
+def _oracle_digest_threads(n, i, seed, nthreads=None):
+    """oracle.digest on contiguous gid shards in parallel threads (ctypes releases the GIL);
+    per-iteration XOR and wrapping sum combine across shards."""
+    import os
+    import threading
+    nthreads = nthreads or max(1, len(os.sched_getaffinity(0)))
+    res = [None] * nthreads
+
+    def work(r):
+        b, c = shard_range(n, r, nthreads)
+        res[r] = oracle.digest(n, i, seed, gid_begin=b, count=c) if c else None
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nthreads)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    x = np.zeros(i, np.uint64)
+    s = np.zeros(i, np.uint64)
+    for rr in res:
+        if rr is not None:
+            x ^= rr[0]
+            s += rr[1]
+    return x, s
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of library-owned device memory (read-only use)."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"data": (ptr, True), "shape": shape, "typestr": "<i8", "version": 3}
+
+
+@pytest.mark.slow
+def test_bench_config_every_ring_slot():
+    """The exact bench.py device-only configuration (numrn = 2^24, numiter = 1000, default
+    kernel and 64 GiB rotating ring, one launch): every output of every iteration still in
+    the ring (the last R = 512 of 1000) folded per iteration into XOR and wrapping sum on
+    the GPU, vs the oracle's digests of the same iterations."""
+    import torch
+    n, i = 1 << 24, 1000
+    h = P.prng_create(n, 0)
+    try:
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        base, pitch, slots, first, end = P.prng_device_ring(h)
+        assert end == i and slots < i
+        ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
+        got_x, got_s = {}, {}
+        for k in range(i - slots, i):
+            row = ring[(first + k) % slots, :n]
+            got_s[k] = int(row.sum().item()) & ((1 << 64) - 1)   # int64 sum wraps mod 2^64
+            v = row.clone()
+            m = v.numel()
+            while m > 1:
+                h2 = m // 2
+                v[:h2] ^= v[m - h2:m]
+                m -= h2
+            got_x[k] = int(v[0].item()) & ((1 << 64) - 1)
+    finally:
+        P.prng_destroy(h)
+    wx, ws = _oracle_digest_threads(n, i, 0)
+    for k in range(i - slots, i):
+        assert got_x[k] == int(wx[k]) and got_s[k] == int(ws[k]), k
