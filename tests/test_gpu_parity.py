@@ -483,7 +483,7 @@ class _DevArray:
     """__cuda_array_interface__ view of library-owned device memory (read-only use)."""
 
     def __init__(self, ptr, shape):
-        self.__cuda_array_interface__ = {"data": (ptr, True), "shape": shape, "typestr": "<i8", "version": 3}
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": shape, "typestr": "<i8", "version": 3}
 
 
 @pytest.mark.slow
