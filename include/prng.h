@@ -114,6 +114,16 @@ int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, pr
 int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch,
                          uint64_t dst_slots, void *stream, prng_err_t *err);
 
+/* a4 + a5, multi-rank form: "each rank generates its own gid range and writes its slice of
+ * the host output directly" (BASELINE north_star).  Generates the next `numiter` iterations
+ * and copies them D2H straight into the caller's host array (no staging buffer, no sink):
+ * iteration k of this call goes to dst[(k mod dst_rows) * dst_pitch + j], j < count.  For
+ * one array shared by all ranks of a node, pass dst = array + gid_begin and dst_pitch =
+ * numrn_total.  dst need not be pinned (it is cudaHostRegister'ed for the call if it is
+ * not).  Blocks until the copies are done; the array is the caller's. */
+int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch,
+                       uint64_t dst_rows, prng_err_t *err);
+
 /* The handle's device ring (device-only mode): base pointer, pitch (u64 elements), number
  * of slots R, and the slot holding iteration 0 of the current prng_init: iteration k
  * (k < last_iter_end, the stream position) was written to slot (iter0_slot + k) mod R and
@@ -247,6 +257,7 @@ int prng_prof_export(uint64_t nevents, const uint32_t *name_id, const double *st
 double prng_probe_memset_gbs(uint64_t bytes, int reps);        /* cudaMemsetAsync write BW  */
 double prng_probe_store_gbs(uint64_t bytes, int reps);         /* pure 32-B store kernel     */
 double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams); /* host link */
+double prng_probe_d2d_sweep_gbs(uint64_t chunk, uint64_t total, int reps); /* copy-engine sweep */
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,7 @@ from ._build import LIB, build as _build_lib
 
 __all__ = [
     "PrngError", "lib", "prng_create", "prng_create_range", "prng_destroy", "prng_init",
-    "prng_generate", "prng_generate_device", "prng_device_ring", "prng_read_slot",
+    "prng_generate", "prng_generate_device", "prng_generate_host", "prng_device_ring", "prng_read_slot",
     "prng_read_state", "prng_set_option", "prng_get_option", "prng_set_streams",
     "prng_strerror", "prng_prof_events", "prng_prof_calc", "prng_event_name",
     "prng_kernel_variants", "prng_kernel_variant_name", "prng_autotune", "prng_probe_memset_gbs",
@@ -87,6 +87,7 @@ def lib():
         "prng_generate": ([vp, u64, vp, vp, E], i32),
         "prng_generate_device": ([vp, u64, vp, u64, u64, vp, E], i32),
         "prng_device_ring": ([vp, ctypes.POINTER(vp), P64, P64, P64, P64, E], i32),
+        "prng_generate_host": ([vp, u64, vp, u64, u64, E], i32),
         "prng_read_slot": ([vp, u64, vp, E], i32),
         "prng_read_state": ([vp, vp, E], i32),
         "prng_set_option": ([vp, i32, i64, E], i32),
@@ -102,6 +103,7 @@ def lib():
         "prng_probe_memset_gbs": ([u64, i32], dbl),
         "prng_probe_store_gbs": ([u64, i32], dbl),
         "prng_probe_d2h_gbs": ([u64, i32, i32, i32], dbl),
+        "prng_probe_d2d_sweep_gbs": ([u64, u64, i32], dbl),
         "prng_sink_null": ([vp, u64, u32, u64, u64, P64], i32),
         "prng_sink_copy": ([vp, u64, u32, u64, u64, P64], i32),
         "prng_sink_digest": ([vp, u64, u32, u64, u64, P64], i32),
@@ -194,6 +196,15 @@ def prng_generate_device(h, numiter: int, dst_ptr: int, dst_pitch: int, dst_slot
     err = prng_err_t()
     _check(lib().prng_generate_device(h, numiter, dst_ptr, dst_pitch, dst_slots, stream or None,
                                       ctypes.byref(err)), err)
+
+
+def prng_generate_host(h, numiter: int, dst: np.ndarray, dst_pitch: int, dst_rows: int, col_offset: int = 0) -> None:
+    """D2H straight into a host array (shared-output multi-rank form): iteration k of the
+    call -> dst.flat[(k % dst_rows) * dst_pitch + col_offset + j]."""
+    assert dst.dtype == np.uint64 and dst.flags["C_CONTIGUOUS"]
+    err = prng_err_t()
+    _check(lib().prng_generate_host(h, numiter, dst.ctypes.data + 8 * col_offset, dst_pitch, dst_rows,
+                                    ctypes.byref(err)), err)
 
 
 def prng_device_ring(h):
@@ -333,6 +344,10 @@ def prng_probe_memset_gbs(nbytes: int, reps: int = 5) -> float:
 
 def prng_probe_store_gbs(nbytes: int, reps: int = 5) -> float:
     return lib().prng_probe_store_gbs(nbytes, reps)
+
+
+def prng_probe_d2d_sweep_gbs(chunk: int, total: int, reps: int = 3) -> float:
+    return lib().prng_probe_d2d_sweep_gbs(chunk, total, reps)
 
 
 def prng_probe_d2h_gbs(nbytes: int, reps: int = 5, pinned: bool = True, nstreams: int = 1) -> float:

@@ -770,15 +770,22 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
 }
 
 // ---------------------------------------------------------------------------- end to end
-static int ensure_e2e(prng *h, uint64_t T, int halves, int kind, bool need_dbuf, prng_err_t *err) {
+// Device double buffer of the end-to-end paths: 2 halves x T slots.
+static int ensure_dbuf(prng *h, uint64_t T, prng_err_t *err) {
     const uint64_t pitch = pitch_for(h->count);
-    if (need_dbuf && (!h->d_buf || h->buf_T != T || h->buf_pitch != pitch)) {
+    if (!h->d_buf || h->buf_T != T || h->buf_pitch != pitch) {
         if (h->d_buf) cudaFree(h->d_buf);
         h->d_buf = nullptr;
         CU(cudaMalloc(&h->d_buf, 2 * T * pitch * sizeof(uint64_t)));
         h->buf_T = T;
         h->buf_pitch = pitch;
     }
+    return PRNG_OK;
+}
+
+static int ensure_e2e(prng *h, uint64_t T, int halves, int kind, bool need_dbuf, prng_err_t *err) {
+    if (need_dbuf)
+        if (int rc = ensure_dbuf(h, T, err)) return rc;
     if (h->h_T != T || h->h_halves < halves || h->h_kind != kind) {
         for (int i = 0; i < 2; ++i) {
             free_host(h->h_kind, h->h_buf[i], h->h_T * h->count * sizeof(uint64_t));
@@ -1013,6 +1020,90 @@ int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, pr
     return ok(err);
 }
 
+// ---------------------------------------------------------------------------- host array
+// a4 + a5, multi-rank form (BASELINE north_star: "each rank generates its own gid range and
+// writes its slice of the host output directly"): D2H straight into the caller's host array
+// -- no staging buffer, no sink.  Iteration k of this call lands in row k mod dst_rows:
+// dst[(k mod dst_rows) * dst_pitch + j], j < count.  For a shared array the caller passes
+// dst = array + gid_begin and dst_pitch = numrn_total, so every rank fills its own columns.
+int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch, uint64_t dst_rows,
+                       prng_err_t *err) {
+    if (int rc = check_handle(h, err, true)) return rc;
+    if (numiter < 1 || !dst || dst_pitch < h->count || dst_rows < 1)
+        return set_err(err, PRNG_EINVAL, "numiter >= 1, dst != NULL, dst_pitch >= count, dst_rows >= 1");
+    if (int rc = ensure_origin(h, err)) return rc;
+    const uint64_t row = h->count * sizeof(uint64_t);
+    uint64_t T = (uint64_t)h->batch_iters;
+    if (T == 0) T = std::max<uint64_t>(1, (256ull << 20) / row);
+    if (int rc = ensure_dbuf(h, T, err)) return rc;
+    T = std::min<uint64_t>(T, numiter);
+    // pin the destination for the DMA engine unless it already is (registered / cudaHostAlloc)
+    const size_t span = ((std::min<uint64_t>(dst_rows, numiter) - 1) * dst_pitch + h->count) * sizeof(uint64_t);
+    cudaPointerAttributes attr;
+    bool registered_here = false;
+    if (cudaPointerGetAttributes(&attr, dst) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        CU(cudaHostRegister(dst, span, cudaHostRegisterDefault));
+        registered_here = true;
+    }
+    const uint64_t nb = (numiter + T - 1) / T, pitch = h->buf_pitch, pos0 = h->pos;
+    auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
+    const int R = 4;
+    cudaEvent_t ev_gen[R], ev_cp[R];
+    for (int i = 0; i < R; ++i) {
+        cudaEventCreateWithFlags(&ev_gen[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming);
+    }
+    int rc = PRNG_OK;
+    const double t0 = now_s();
+    for (uint64_t j = 0; j < nb && !rc; ++j) {
+        // gen(j) into device half j%2, after copy(j-2) has drained it (WAR, A15)
+        if (j >= 2 && cudaStreamWaitEvent(h->s_gen, ev_cp[(j - 2) % R], 0) != cudaSuccess) {
+            rc = set_err(err, PRNG_ECUDA, "cudaStreamWaitEvent");
+            break;
+        }
+        rc = launch_batch(h, h->d_buf, pitch, 2 * T, (j & 1) * T, iters_of(j), pos0 + j * T == 0, h->s_gen, err);
+        if (rc) break;
+        cudaEventRecord(ev_gen[j % R], h->s_gen);
+        // copy(j): rows (pos0 + j*T + t) mod dst_rows, split where the host ring wraps
+        cudaStreamWaitEvent(h->s_copy, ev_gen[j % R], 0);
+        if ((rc = prof_begin(h, h->s_copy, PRNG_EV_READ_BUFFER, err))) break;
+        uint64_t t = 0;
+        while (t < iters_of(j)) {
+            const uint64_t r0 = (j * T + t) % dst_rows;  // destination row of call iteration j*T + t
+            const uint64_t nrows = std::min<uint64_t>(iters_of(j) - t, dst_rows - r0);
+            const cudaError_t e = cudaMemcpy2DAsync(dst + r0 * dst_pitch, dst_pitch * sizeof(uint64_t),
+                                                    h->d_buf + ((j & 1) * T + t) * pitch, pitch * sizeof(uint64_t), row,
+                                                    nrows, cudaMemcpyDeviceToHost, h->s_copy);
+            if (e != cudaSuccess) {
+                rc = set_err(err, PRNG_ECUDA, "cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
+                break;
+            }
+            t += nrows;
+        }
+        if (rc) break;
+        if ((rc = prof_end(h, h->s_copy, err))) break;
+        cudaEventRecord(ev_cp[j % R], h->s_copy);
+        // keep at most two batches in flight per stream (the event ring has R = 4 entries)
+        if (j >= 2) cudaEventSynchronize(ev_cp[(j - 2) % R]);
+    }
+    cudaStreamSynchronize(h->s_gen);
+    const cudaError_t e = cudaStreamSynchronize(h->s_copy);
+    for (int i = 0; i < R; ++i) {
+        cudaEventDestroy(ev_gen[i]);
+        cudaEventDestroy(ev_cp[i]);
+    }
+    if (registered_here) cudaHostUnregister(dst);
+    if (!rc && e != cudaSuccess) rc = set_err(err, PRNG_ECUDA, "copy stream: %s", cudaGetErrorString(e));
+    if (rc) {
+        h->poisoned = true;
+        return rc;
+    }
+    h->pos = pos0 + numiter;
+    h->wall_s += now_s() - t0;
+    return ok(err);
+}
+
 int prng_device_ring(const prng_t *h, uint64_t **base, uint64_t *pitch, uint64_t *slots, uint64_t *iter0_slot,
                      uint64_t *last_iter_end, prng_err_t *err) {
     if (!h || !base || !pitch || !slots || !iter0_slot || !last_iter_end)
@@ -1154,6 +1245,38 @@ double prng_probe_store_gbs(uint64_t bytes, int reps) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(p);
+    return cudaGetLastError() == cudaSuccess ? best : -1;
+}
+
+// Copy-engine write probe: a `chunk`-byte (L2-resident) source copied D2D over a `total`-byte
+// destination, chunk by chunk (cudaMemcpyAsync), i.e. the DRAM sees a sequential write
+// sweep fed from L2.  Returns destination GB/s (best of reps).
+double prng_probe_d2d_sweep_gbs(uint64_t chunk, uint64_t total, int reps) {
+    void *src = nullptr, *dst = nullptr;
+    if (cudaMalloc(&src, chunk) != cudaSuccess) return -1;
+    if (cudaMalloc(&dst, total) != cudaSuccess) {
+        cudaFree(src);
+        return -1;
+    }
+    cudaMemset(src, 3, chunk);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0;
+    for (int r = 0; r < reps + 1; ++r) {
+        cudaEventRecord(a);
+        for (uint64_t off = 0; off + chunk <= total; off += chunk)
+            cudaMemcpyAsync((char *)dst + off, src, chunk, cudaMemcpyDeviceToDevice);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (r) best = std::max(best, (total / chunk) * (double)chunk / (ms * 1e-3) / 1e9);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(src);
+    cudaFree(dst);
     return cudaGetLastError() == cudaSuccess ? best : -1;
 }
 

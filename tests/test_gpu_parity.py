@@ -517,3 +517,79 @@ def test_bench_config_every_ring_slot():
     wx, ws = _oracle_digest_threads(n, i, 0)
     for k in range(i - slots, i):
         assert got_x[k] == int(wx[k]) and got_s[k] == int(ws[k]), k
+
+
+# ---------------------------------------------------------------- shared host output (north_star e)
+def test_generate_host_shards_fill_one_array():
+    """Each 'rank' (one handle per gid shard) writes its columns of one host array directly."""
+    n, i, world = 10007, 9, 3
+    arr = np.zeros((i, n), np.uint64)
+    for r in range(world):
+        b, c = shard_range(n, r, world)
+        h = P.prng_create_range(n, SEED_PARITY, b, c)
+        try:
+            P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 2)
+            P.prng_init(h)
+            P.prng_generate_host(h, i, arr, n, i, col_offset=b)
+        finally:
+            P.prng_destroy(h)
+    assert np.array_equal(arr, oracle.stream(n, i, SEED_PARITY))
+
+
+def test_generate_host_row_ring_and_continuation():
+    """dst_rows < numiter wraps; a second call continues the stream into its own rows."""
+    n, i, rows = 3000, 11, 4
+    want = oracle.stream(n, 2 * i, 4)
+    arr = np.zeros((rows, n), np.uint64)
+    h = P.prng_create(n, 4)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 3)
+        P.prng_init(h)
+        P.prng_generate_host(h, i, arr, n, rows)
+        for k in range(i - rows, i):
+            assert np.array_equal(arr[k % rows], want[k])
+        P.prng_generate_host(h, i, arr, n, rows)
+        for k in range(i - rows, i):
+            assert np.array_equal(arr[k % rows], want[i + k])
+    finally:
+        P.prng_destroy(h)
+
+
+def _rank_writes_shm(rank, world, n, i, shm_name):
+    import numpy as _np
+    from multiprocessing import shared_memory
+    import paper_1609_01257_b200 as _P
+    from workloads import shard_range as _sr
+    shm = shared_memory.SharedMemory(name=shm_name)
+    try:
+        arr = _np.ndarray((i, n), dtype=_np.uint64, buffer=shm.buf)
+        b, c = _sr(n, rank, world)
+        h = _P.prng_create_range(n, 7, b, c, 0)
+        try:
+            _P.prng_init(h)
+            _P.prng_generate_host(h, i, arr, n, i, col_offset=b)
+        finally:
+            _P.prng_destroy(h)
+        del arr
+    finally:
+        shm.close()
+
+
+def test_two_processes_write_one_shared_host_array():
+    """Two processes (ranks) on cuda:0, one POSIX shared-memory output array: each D2H's its
+    gid columns straight into it; the parent sees the single-device stream."""
+    import multiprocessing as mp
+    from multiprocessing import shared_memory
+    n, i, world = 4099, 6, 2
+    shm = shared_memory.SharedMemory(create=True, size=8 * n * i)
+    try:
+        ctx = mp.get_context("spawn")
+        ps = [ctx.Process(target=_rank_writes_shm, args=(r, world, n, i, shm.name)) for r in range(world)]
+        [p.start() for p in ps]
+        [p.join(timeout=300) for p in ps]
+        assert all(p.exitcode == 0 for p in ps)
+        arr = np.ndarray((i, n), dtype=np.uint64, buffer=shm.buf).copy()
+        assert np.array_equal(arr, oracle.stream(n, i, 7))
+    finally:
+        shm.close()
+        shm.unlink()
