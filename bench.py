@@ -343,10 +343,28 @@ def run_ours(a, D):
                    "rng_read_overlap_s": ov[1, 2],
                    "rng_hidden_frac": (ov[1, 2] / agg[1]) if agg[1] else None,
                    "copy_busy_frac": agg[2] / w if w else None, "effective_s": calc["effective"], "wall_s": w}}
+        # the multi-rank form: D2H straight into a host array (ring of 2T rows, pinned by
+        # torch), no staging buffer and no sink -- each rank writes its slice directly
+        import numpy as np
+        T = max(1, (256 << 20) // (8 * cnt))
+        rows = 2 * T
+        harr = torch.empty((rows, cnt), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        P.prng_init(h)
+        P.prng_generate_host(h, min(a.numiter, rows), harr, cnt, rows)  # warm-up
+        D.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        P.prng_init(h)
+        P.prng_generate_host(h, a.numiter, harr, cnt, rows)
+        dt = D.max(time.perf_counter() - t0)
+        e2e["host_array"] = {"value": numrn * a.numiter / dt, "unit": "numbers/s",
+                             "gbs": 8 * numrn * a.numiter / dt / 1e9, "rows": rows,
+                             "how": "prng_generate_host: D2H straight into a pinned host array (ring of rows)"}
+        del harr
     probes = None
     if not a.no_probes and D.rank == 0:
-        probes = {"memset_write_gbs": P.prng_probe_memset_gbs(4 << 30, 5),
-                  "store_kernel_write_gbs": P.prng_probe_store_gbs(4 << 30, 5),
+        probes = {"memset_write_gbs": P.prng_probe_memset_gbs(32 << 30, 3),
+                  "store_kernel_write_gbs": P.prng_probe_store_gbs(32 << 30, 3),
                   "d2h_pinned_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 1),
                   "d2h_pinned_2streams_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 2)}
         roofline["frac_of_same_box_memset"] = achieved / probes["memset_write_gbs"]
