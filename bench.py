@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--ref-numiter", type=int, default=8, help="--impl reference: numiter per step sample")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--output", type=int, default=0, help="0 = the state (paper); 1 = xorshift64* scrambled (NEXT-3)")
+    ap.add_argument("--no-numa-bind", action="store_true", help="keep the process's CPU affinity")
     ap.add_argument("--device-mod", type=int, default=0,
                     help="TEST ONLY: map local rank r to GPU r %% K (several ranks per GPU; timings meaningless)")
     return ap.parse_args()
@@ -163,6 +164,25 @@ class Clocks:
                 "samples": len(self.rows), "busy_samples": len(busy), "source": "nvml 5 ms"}
 
 
+def bind_to_gpu_cpus(dev):
+    """Pin this rank to the CPUs NVML reports as local to its GPU, before any pinned host
+    buffer is allocated, so the D2H targets NUMA-local memory."""
+    try:
+        import pynvml as N
+        N.nvmlInit()
+        hd = N.nvmlDeviceGetHandleByIndex(dev)
+        ncpu = os.cpu_count() or 1
+        words = N.nvmlDeviceGetCpuAffinity(hd, (ncpu + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(ncpu))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return {"cpus": len(cpus), "of": ncpu}
+    except Exception as e:  # noqa: BLE001
+        return {"error": repr(e)}
+    return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -243,6 +263,7 @@ def run_ours(a, D):
 
     dev = D.local % a.device_mod if a.device_mod > 0 else D.local
     torch.cuda.set_device(dev)
+    numa = bind_to_gpu_cpus(dev) if not a.no_numa_bind else None
     numrn = a.numrn_total or a.numrn_per_gpu * D.world
     gb, cnt = shard_range(numrn, D.rank, D.world)
     gen = torch.cuda.Stream()
@@ -397,6 +418,7 @@ def run_ours(a, D):
                                     f"numrn={numrn} total ({cnt} per GPU, gid-range sharded) x numiter={a.numiter}"),
                        "numrn": numrn, "numiter": a.numiter, "seed": a.seed, "parallelism": f"gid-shard{D.world}",
                        "output": ["state (paper)", "xorshift64* scrambled"][a.output],
+                       "numa_bind": numa,
                        "l2": "output through a 64 GiB rotating ring per GPU (> 500x L2; no address rewritten "
                              "within 64 GiB, see profiles/r1_ring_absorption.md); no flush needed"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
