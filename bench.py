@@ -389,6 +389,7 @@ def run_ours(a, D):
                   "d2h_pinned_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 1),
                   "d2h_pinned_2streams_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 2)}
         roofline["frac_of_same_box_memset"] = achieved / probes["memset_write_gbs"]
+        roofline["frac_of_same_box_store_kernel"] = achieved / probes["store_kernel_write_gbs"]
         if e2e:
             e2e["roofline"] = {"bound": "host-link", "achieved": e2e["d2h_gbs_per_gpu"],
                                "peak": probes["d2h_pinned_gbs"], "unit": "GB/s",

@@ -256,6 +256,8 @@ int prng_prof_export(uint64_t nevents, const uint32_t *name_id, const double *st
  * error.  bytes: buffer size. */
 double prng_probe_memset_gbs(uint64_t bytes, int reps);        /* cudaMemsetAsync write BW  */
 double prng_probe_store_gbs(uint64_t bytes, int reps);         /* pure 32-B store kernel     */
+/* pattern 0 index, 1 zeros, 2 pseudo-random; warps_per_sm 0 = full occupancy */
+double prng_probe_store_pattern_gbs(uint64_t bytes, int reps, int pattern, int warps_per_sm);
 double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams); /* host link */
 double prng_probe_d2d_sweep_gbs(uint64_t chunk, uint64_t total, int reps); /* copy-engine sweep */
 

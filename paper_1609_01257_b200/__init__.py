@@ -102,6 +102,7 @@ def lib():
         "prng_prof_export": ([u64, vp, vp, vp, u32, vp, vp, ctypes.c_char_p, E], i32),
         "prng_probe_memset_gbs": ([u64, i32], dbl),
         "prng_probe_store_gbs": ([u64, i32], dbl),
+        "prng_probe_store_pattern_gbs": ([u64, i32, i32, i32], dbl),
         "prng_probe_d2h_gbs": ([u64, i32, i32, i32], dbl),
         "prng_probe_d2d_sweep_gbs": ([u64, u64, i32], dbl),
         "prng_sink_null": ([vp, u64, u32, u64, u64, P64], i32),
@@ -348,6 +349,10 @@ def prng_probe_store_gbs(nbytes: int, reps: int = 5) -> float:
 
 def prng_probe_d2d_sweep_gbs(chunk: int, total: int, reps: int = 3) -> float:
     return lib().prng_probe_d2d_sweep_gbs(chunk, total, reps)
+
+
+def prng_probe_store_pattern_gbs(nbytes: int, reps: int = 3, pattern: int = 0, warps_per_sm: int = 0) -> float:
+    return lib().prng_probe_store_pattern_gbs(nbytes, reps, pattern, warps_per_sm)
 
 
 def prng_probe_d2h_gbs(nbytes: int, reps: int = 5, pinned: bool = True, nstreams: int = 1) -> float:

@@ -1221,7 +1221,9 @@ double prng_probe_memset_gbs(uint64_t bytes, int reps) {
     return cudaGetLastError() == cudaSuccess ? best : -1;
 }
 
-double prng_probe_store_gbs(uint64_t bytes, int reps) {
+double prng_probe_store_gbs(uint64_t bytes, int reps) { return prng_probe_store_pattern_gbs(bytes, reps, 0, 0); }
+
+double prng_probe_store_pattern_gbs(uint64_t bytes, int reps, int pattern, int warps_per_sm) {
     uint64_t *p = nullptr;
     bytes &= ~31ull;
     if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
@@ -1235,7 +1237,10 @@ double prng_probe_store_gbs(uint64_t bytes, int reps) {
     double best = 0;
     for (int r = 0; r < reps + 1; ++r) {
         cudaEventRecord(a);
-        prngk::store_probe_kernel<<<sms * std::max(bps, 1), kBlock>>>(p, bytes / 32);
+        if (warps_per_sm > 0)
+            prngk::store_probe_kernel<<<sms, 32 * std::min(warps_per_sm, 32), 0>>>(p, bytes / 32, pattern);
+        else
+            prngk::store_probe_kernel<<<sms * std::max(bps, 1), kBlock>>>(p, bytes / 32, pattern);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms = 0;

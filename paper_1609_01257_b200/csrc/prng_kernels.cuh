@@ -488,11 +488,21 @@ __global__ void __launch_bounds__(256) batch_kernel_tma(BatchArgs a) {
 }
 
 // ---------------------------------------------------------------- roofline probe kernel
-// Pure 32-byte streaming store of a constant pattern: the same-box write ceiling.
-__global__ void __launch_bounds__(256) store_probe_kernel(uint64_t *p, uint64_t n4) {
+// Pure 32-byte grid-stride store stream: the same-box SM write ceiling.  pattern 0: the
+// index (i, i+1, ...), 1: zeros, 2: pseudo-random (xorshift64 of the index) -- to see
+// whether the data values change the write rate (e.g. compression of constant data).
+__global__ void __launch_bounds__(256) store_probe_kernel(uint64_t *p, uint64_t n4, int pattern) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride)
-        st_v4<0>(p + 4 * i, i, i + 1, i + 2, i + 3);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        if (pattern == 1) {
+            st_v4<0>(p + 4 * i, 0, 0, 0, 0);
+        } else if (pattern == 2) {
+            const uint64_t x = xorshift64(i * 0x9E3779B97F4A7C15ull + 1);
+            st_v4<0>(p + 4 * i, x, x ^ 0xA5A5A5A5A5A5A5A5ull, x * 3, ~x);
+        } else {
+            st_v4<0>(p + 4 * i, i, i + 1, i + 2, i + 3);
+        }
+    }
 }
 
 }  // namespace prngk
