@@ -79,10 +79,19 @@ __device__ __forceinline__ uint64_t emit(uint64_t x) {
 // ---------------------------------------------------------------- vector memory helpers
 // POLICY 0: default write-back; 1: .cs (streaming, evict-first) -- the output is never
 // re-read by the SMs, only by the copy engine.
+// POLICY 2: L2 evict_first cache-hint policy; 3: L1::no_allocate.
 template <int POLICY>
 __device__ __forceinline__ void st_v4(uint64_t *p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
     if constexpr (POLICY == 1)
         asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+    else if constexpr (POLICY == 2)
+        asm volatile(
+            "{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+            "st.global.L2::cache_hint.v4.u64 [%0], {%1, %2, %3, %4}, pol; }" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d)
+            : "memory");
+    else if constexpr (POLICY == 3)
+        asm volatile("st.global.L1::no_allocate.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
+                     "l"(d) : "memory");
     else
         asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
 }
@@ -90,6 +99,12 @@ template <int POLICY>
 __device__ __forceinline__ void st_v2(uint64_t *p, uint64_t a, uint64_t b) {
     if constexpr (POLICY == 1)
         asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+    else if constexpr (POLICY == 2)
+        asm volatile(
+            "{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+            "st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, pol; }" ::"l"(p), "l"(a), "l"(b) : "memory");
+    else if constexpr (POLICY == 3)
+        asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
     else
         asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
