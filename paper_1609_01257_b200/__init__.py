@@ -177,19 +177,26 @@ def prng_generate(h, numiter: int, sink=None, user=None) -> None:
     callable f(iter_begin, iters, gid_begin, count, ndarray[iters, count]) -> int."""
     err = prng_err_t()
     keep = None
+    raised = []
     if sink is None:
         sp = None
     elif isinstance(sink, int):
         sp = sink
     else:
         def tramp(_u, k0, it, g0, cnt, data):
-            arr = np.ctypeslib.as_array(data, shape=(it * cnt,)).reshape(it, cnt)
-            return int(sink(k0, it, g0, cnt, arr) or 0)
+            try:
+                arr = np.ctypeslib.as_array(data, shape=(it * cnt,)).reshape(it, cnt)
+                return int(sink(k0, it, g0, cnt, arr) or 0)
+            except BaseException as e:  # noqa: BLE001 -- abort generation, re-raise below
+                raised.append(e)
+                return 1
         keep = SINK_FN(tramp)
         sp = ctypes.cast(keep, vp).value
     up = ctypes.cast(ctypes.pointer(user), vp).value if isinstance(user, ctypes.Structure) else user
     rc = lib().prng_generate(h, numiter, sp, up, ctypes.byref(err))
     del keep
+    if raised:
+        raise raised[0]
     _check(rc, err)
 
 

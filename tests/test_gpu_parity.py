@@ -593,3 +593,21 @@ def test_two_processes_write_one_shared_host_array():
     finally:
         shm.close()
         shm.unlink()
+
+
+def test_python_sink_exception_propagates():
+    """A Python sink that raises aborts generation (PRNG_ESINK inside) and the exception
+    reaches the caller; the handle is poisoned until prng_init."""
+    h = P.prng_create(100, 0)
+    try:
+        P.prng_init(h)
+
+        def bad(*a):
+            raise KeyError("consumer failed")
+        with pytest.raises(KeyError):
+            P.prng_generate(h, 5, bad)
+        with pytest.raises(P.PrngError) as e:
+            P.prng_generate(h, 1, P.SINK_NULL)
+        assert e.value.code == P.PRNG_ESTATE
+    finally:
+        P.prng_destroy(h)
