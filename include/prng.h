@@ -93,6 +93,12 @@ int prng_set_streams(prng_t *h, void *gen_stream, void *copy_stream, prng_err_t 
  * position is reset to iteration 0 (the next iteration emitted is the seeds themselves). */
 int prng_init(prng_t *h, prng_err_t *err);
 
+/* Checkpoint / resume: re-seed (as prng_init) and position the stream so that the next
+ * iteration emitted is `iteration` -- the same values a run from prng_init would emit
+ * from there on -- in O(log iteration) work: xorshift is GF(2)-linear, so
+ * iteration - 1 steps are one 64x64 bit-matrix product per work-item (readings A5, P8). */
+int prng_seek(prng_t *h, uint64_t iteration, prng_err_t *err);
+
 /* a2-a5 -- emit the next `numiter` iterations (numiter >= 1).
  *  sink != NULL (end to end): batches of T iterations are generated into a device ring,
  *    copied D2H on a side stream into a pinned host double buffer and handed to `sink`

@@ -16,7 +16,7 @@ from ._build import LIB, build as _build_lib
 
 __all__ = [
     "PrngError", "lib", "prng_create", "prng_create_range", "prng_destroy", "prng_init",
-    "prng_generate", "prng_generate_device", "prng_generate_host", "prng_device_ring", "prng_read_slot",
+    "prng_generate", "prng_generate_device", "prng_generate_host", "prng_seek", "prng_device_ring", "prng_read_slot",
     "prng_read_state", "prng_set_option", "prng_get_option", "prng_set_streams",
     "prng_strerror", "prng_prof_events", "prng_prof_calc", "prng_event_name",
     "prng_kernel_variants", "prng_kernel_variant_name", "prng_autotune", "prng_probe_memset_gbs",
@@ -84,6 +84,7 @@ def lib():
         "prng_destroy": ([vp], None),
         "prng_set_streams": ([vp, vp, vp, E], i32),
         "prng_init": ([vp, E], i32),
+        "prng_seek": ([vp, u64, E], i32),
         "prng_generate": ([vp, u64, vp, vp, E], i32),
         "prng_generate_device": ([vp, u64, vp, u64, u64, vp, E], i32),
         "prng_device_ring": ([vp, ctypes.POINTER(vp), P64, P64, P64, P64, E], i32),
@@ -170,6 +171,12 @@ def prng_set_streams(h, gen_stream: int, copy_stream: int) -> None:
 def prng_init(h) -> None:
     err = prng_err_t()
     _check(lib().prng_init(h, ctypes.byref(err)), err)
+
+
+def prng_seek(h, iteration: int) -> None:
+    """Re-seed and jump so that the next iteration emitted is `iteration` (checkpoint/resume)."""
+    err = prng_err_t()
+    _check(lib().prng_seek(h, iteration, ctypes.byref(err)), err)
 
 
 def prng_generate(h, numiter: int, sink=None, user=None) -> None:

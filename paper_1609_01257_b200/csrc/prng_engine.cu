@@ -296,7 +296,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
             }
             const uint64_t e = first_is_state ? 0 : 1;
             if (h->jump_key[0] != C || h->jump_key[1] != L || h->jump_key[2] != e) {
-                prngk::jump_columns_kernel<<<1, 64, 0, s>>>(h->d_jump, (uint32_t)C, (uint32_t)L, (uint32_t)e);
+                prngk::jump_columns_kernel<<<1, 64, 0, s>>>(h->d_jump, (uint32_t)C, (uint64_t)L, (uint32_t)e);
                 CU(cudaGetLastError());
                 h->jump_key[0] = C;
                 h->jump_key[1] = L;
@@ -618,6 +618,35 @@ int prng_init(prng_t *h, prng_err_t *err) {
         CU(cudaStreamSynchronize(h->s_gen));
         h->wall_s += now_s() - t0;
     }
+    return ok(err);
+}
+
+// ---------------------------------------------------------------------------- seek
+// Checkpoint / resume ("the state after iteration k is output k"): position
+// the stream so that the next iteration emitted is `iteration`, without generating the
+// ones before it -- the seeds (a1) jumped (iteration - 1) xorshift steps ahead by one
+// GF(2) mat-vec per work-item with T^(iteration-1) built by binary exponentiation
+// (xs is linear, P8).  seek(0) == prng_init.
+int prng_seek(prng_t *h, uint64_t iteration, prng_err_t *err) {
+    if (int rc = prng_init(h, err)) return rc;
+    if (iteration == 0) return ok(err);
+    if (h->jump_cap < 2) {
+        if (h->d_jump) cudaFree(h->d_jump);
+        h->d_jump = nullptr;
+        h->jump_cap = 0;
+        CU(cudaMalloc(&h->d_jump, 2 * 64 * sizeof(uint64_t)));
+        h->jump_cap = 2;
+    }
+    h->jump_key[0] = 0;  // the chunk cache no longer matches
+    // J_1 = T^L * T^0 with L = iteration - 1
+    prngk::jump_columns_kernel<<<1, 64, 0, h->s_gen>>>(h->d_jump, 2u, iteration - 1, 0u);
+    CU(cudaGetLastError());
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((h->count + kBlock - 1) / kBlock,
+                                                                     (uint64_t)h->num_sms * 8));
+    prngk::jump_states_kernel<<<(unsigned)blocks, kBlock, 0, h->s_gen>>>(h->d_state, h->count, h->d_jump + 64);
+    CU(cudaGetLastError());
+    h->pos = iteration;  // state == out[iteration - 1]: the next launch steps, then emits
+    if (h->blocking) CU(cudaStreamSynchronize(h->s_gen));
     return ok(err);
 }
 

@@ -199,14 +199,14 @@ __device__ __forceinline__ uint64_t gf2_matvec_smem(const uint64_t *M, uint64_t 
     return y;
 }
 
-__global__ void __launch_bounds__(64) jump_columns_kernel(uint64_t *jump, uint32_t C, uint32_t L, uint32_t e) {
+__global__ void __launch_bounds__(64) jump_columns_kernel(uint64_t *jump, uint32_t C, uint64_t L, uint32_t e) {
     __shared__ uint64_t B[64], R[64];
     const uint32_t i = threadIdx.x;
     const uint64_t t_col = xorshift64(1ull << i);  // T e_i
     B[i] = t_col;
     R[i] = 1ull << i;  // identity
     __syncthreads();
-    for (uint32_t k = L; k; k >>= 1) {
+    for (uint64_t k = L; k; k >>= 1) {
         if (k & 1) {
             const uint64_t r = gf2_matvec_smem(B, R[i]);  // R = B R
             __syncthreads();
@@ -225,6 +225,17 @@ __global__ void __launch_bounds__(64) jump_columns_kernel(uint64_t *jump, uint32
         col = gf2_matvec_smem(R, col);
         jump[(uint64_t)c * 64 + i] = col;
     }
+}
+
+// Checkpoint / resume: state[g] = J * state[g] for every gid (J = T^k from
+// jump_columns_kernel), i.e. k xorshift steps in one GF(2) mat-vec per state.
+__global__ void __launch_bounds__(256) jump_states_kernel(uint64_t *state, uint64_t count, const uint64_t *J) {
+    __shared__ uint64_t Js[64];
+    if (threadIdx.x < 64) Js[threadIdx.x] = J[threadIdx.x];
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < count; g += stride)
+        state[g] = gf2_matvec_smem(Js, state[g]);
 }
 
 // One work unit of a warp: the gids of one piece over iterations [t_begin, t_begin + t_count).

@@ -2,7 +2,7 @@
  * rng_b200 -- NEXT-1: the paper's example program on the B200 path (§5).
  *
  *   rng_b200 n i [--seed S] [--mode O2|O1|O3|S0|S1] [--batch T] [--device D]
- *                [--star] [--profile] [--export FILE]
+ *                [--star] [--start K] [--profile] [--export FILE]
  *
  * "a standalone program which outputs random numbers in binary format to the standard
  * output ... The program accepts two parameters: a) n, the quantity of 64-bit (8-byte)
@@ -28,7 +28,8 @@
 static void usage(FILE *f) {
     fprintf(f,
             "usage: rng_b200 n i [--seed S] [--mode O2|O1|O3|S0|S1] [--batch T] [--device D]\n"
-            "                [--star] [--profile] [--export FILE]\n"
+            "                [--star] [--start K] [--profile] [--export FILE]\n"
+            "  --start K  resume: emit iterations K .. K+i-1 (GF(2) jump-ahead, no replay)\n"
             "  --star  xorshift64*-scrambled output (state * 0x2545F4914F6CDD1D)\n"
             "  n  64-bit random values per iteration (1 .. 2^32)\n"
             "  i  iterations (>= 1); writes 8*n*i bytes to stdout\n");
@@ -64,7 +65,7 @@ static int sink_stdout(void *user, uint64_t iter_begin, uint32_t iters, uint64_t
 }
 
 int main(int argc, char **argv) {
-    uint64_t n = 0, iters = 0, seed = 0, batch = 0;
+    uint64_t n = 0, iters = 0, seed = 0, batch = 0, start = 0;
     int mode = PRNG_MODE_OVERLAP2, device = -1, profile = 0, npos = 0, star = 0;
     const char *export_path = NULL;
     for (int a = 1; a < argc; ++a) {
@@ -74,6 +75,8 @@ int main(int argc, char **argv) {
             return 0;
         } else if (!strcmp(s, "--seed") && a + 1 < argc) {
             if (parse_u64(argv[++a], &seed)) return usage(stderr), 2;
+        } else if (!strcmp(s, "--start") && a + 1 < argc) {
+            if (parse_u64(argv[++a], &start)) return usage(stderr), 2;
         } else if (!strcmp(s, "--batch") && a + 1 < argc) {
             if (parse_u64(argv[++a], &batch)) return usage(stderr), 2;
         } else if (!strcmp(s, "--device") && a + 1 < argc) {
@@ -116,7 +119,7 @@ int main(int argc, char **argv) {
     if (!rc) rc = prng_set_option(h, PRNG_OPT_BATCH_ITERS, (int64_t)batch, &err);
     if (!rc) rc = prng_set_option(h, PRNG_OPT_PROFILE, profile, &err);
     if (!rc) rc = prng_set_option(h, PRNG_OPT_OUTPUT, star, &err);
-    if (!rc) rc = prng_init(h, &err);
+    if (!rc) rc = start ? prng_seek(h, start, &err) : prng_init(h, &err);
     if (!rc) rc = prng_generate(h, iters, sink_stdout, NULL, &err);
     if (rc) {
         fprintf(stderr, "rng_b200: %s: %s\n", prng_strerror(rc), err.msg);

@@ -83,3 +83,12 @@ def test_cli_closed_pipe_is_an_error(cli):
     p.stdout.read(4096)
     p.stdout.close()
     assert p.wait(timeout=120) == 1
+
+
+@pytest.mark.gpu
+def test_cli_resume_from_iteration(cli):
+    """--start K emits iterations K .. K+i-1: the tail of the uninterrupted stream."""
+    r = run(cli, 1000, 5, "--start", 12)
+    assert r.returncode == 0, r.stderr
+    got = np.frombuffer(r.stdout, dtype="<u8").reshape(5, 1000)
+    assert np.array_equal(got, oracle.stream(1000, 17, 0)[12:])

@@ -611,3 +611,61 @@ def test_python_sink_exception_propagates():
         assert e.value.code == P.PRNG_ESTATE
     finally:
         P.prng_destroy(h)
+
+
+# ---------------------------------------------------------------- checkpoint / resume (prng_seek)
+@pytest.mark.parametrize("k", [0, 1, 2, 7, 1000, 65537])
+def test_seek_resumes_the_stream(k):
+    n, m = 333, 600
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_seek(h, k)
+        out = np.zeros((m, n), np.uint64)
+        P.prng_generate(h, m, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, k, m, 0))
+    finally:
+        P.prng_destroy(h)
+    assert np.array_equal(out, oracle.stream(n, k + m, SEED_PARITY)[k:])
+
+
+def _xs_pow_columns(k):
+    """Columns of T^k for the ORACLE's xs by binary exponentiation over GF(2) (test-side)."""
+    cols = [oracle.xorshift64(1 << j) for j in range(64)]
+
+    def apply(M, x):
+        y = 0
+        for j in range(64):
+            if (x >> j) & 1:
+                y ^= M[j]
+        return y
+
+    R = [1 << j for j in range(64)]
+    B = cols
+    while k:
+        if k & 1:
+            R = [apply(B, c) for c in R]
+        B = [apply(B, c) for c in B]
+        k >>= 1
+    return R, apply
+
+
+def test_seek_far_ahead():
+    """k = 2^40 + 5: no oracle can step there; the expected state is xs^(k-1)(seed64) by a
+    test-side GF(2) power of the oracle's own xs, then the stream continues by the oracle."""
+    k = (1 << 40) + 5
+    n, m = 64, 3
+    R, apply = _xs_pow_columns(k - 1)
+    h = P.prng_create(n, 1)
+    try:
+        P.prng_seek(h, k)
+        st = P.prng_read_state(h, n)
+        out = np.zeros((m, n), np.uint64)
+        P.prng_generate(h, m, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, k, m, 0))
+    finally:
+        P.prng_destroy(h)
+    for g in range(n):
+        want = apply(R, oracle.seed64(g, 1))
+        assert int(st[g]) == want
+        x = want
+        for t in range(m):
+            x = oracle.xorshift64(x)
+            assert int(out[t, g]) == x
