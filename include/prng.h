@@ -166,9 +166,11 @@ enum prng_option {
     PRNG_OPT_TIME_PARALLEL = 11, /* 1 (default): when numrn is too small to fill the GPU, cut
                                   a launch's iterations into chunks started by GF(2)
                                   jump-ahead (xs^k is linear: a 64x64 bit matrix); 0: off */
-    PRNG_OPT_BLOCKING = 12     /* 1 (default): device-only prng_generate returns when the work
+    PRNG_OPT_BLOCKING = 12,    /* 1 (default): device-only prng_generate returns when the work
                                   is done; 0: returns after enqueueing on the generation
                                   stream (synchronise the stream before reading results)   */
+    PRNG_OPT_CTA_WARPS = 13    /* warps per CTA of the batch kernels (1..8); 0 = auto: one
+                                  CTA per SM when <= 8 warps per SM are used               */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two

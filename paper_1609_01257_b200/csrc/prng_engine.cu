@@ -151,7 +151,7 @@ struct prng {
 
     // options
     int mode = PRNG_MODE_OVERLAP2;
-    int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0, ring_pad = 0;
+    int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0, ring_pad = 0, cta_warps = 0;
     unsigned long long *trace = nullptr;  // PRNG_OPT_TRACE_PTR (diagnostic variant only)
 
     int profile = 0, kernel = 0, output = 0, blocking = 1;
@@ -315,6 +315,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // ceil(warps / SMs) warps, else 256-thread CTAs.
     uint64_t wpb = kBlock / 32;
     if (warps <= (uint64_t)h->num_sms * wpb) wpb = std::max<uint64_t>(1, (warps + h->num_sms - 1) / h->num_sms);
+    if (h->cta_warps > 0 && v.stages == 0) wpb = (uint64_t)h->cta_warps;  // PRNG_OPT_CTA_WARPS
     uint64_t blocks = (warps + wpb - 1) / wpb;
     const uint64_t C = (uint64_t)v.cluster;
     if (C > 1) {
@@ -544,6 +545,10 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
         case PRNG_OPT_TIME_PARALLEL:
             h->time_parallel = value ? 1 : 0;
             break;
+        case PRNG_OPT_CTA_WARPS:
+            if (value < 0 || value > kBlock / 32) return set_err(err, PRNG_EINVAL, "bad CTA warps");
+            h->cta_warps = value;
+            break;
         case PRNG_OPT_OUTPUT:
             if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad output transform");
             if (value == 1 && h->kernel >= kNumStar)
@@ -584,6 +589,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_KERNEL: *value = h->kernel; break;
         case PRNG_OPT_OUTPUT: *value = h->output; break;
         case PRNG_OPT_TIME_PARALLEL: *value = h->time_parallel; break;
+        case PRNG_OPT_CTA_WARPS: *value = h->cta_warps; break;
         case PRNG_OPT_GRID_WARPS: *value = h->grid_warps; break;
         case PRNG_OPT_RING_PAD: *value = h->ring_pad; break;
         case PRNG_OPT_HOST_MEM: *value = h->host_mem; break;
