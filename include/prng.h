@@ -268,6 +268,9 @@ double prng_probe_store_gbs(uint64_t bytes, int reps);         /* pure 32-B stor
 double prng_probe_store_pattern_gbs(uint64_t bytes, int reps, int pattern, int warps_per_sm);
 double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams); /* host link */
 double prng_probe_d2d_sweep_gbs(uint64_t chunk, uint64_t total, int reps); /* copy-engine sweep */
+/* research probe of SM store patterns (modes in prng_kernels.cuh store_pattern_kernel) */
+double prng_probe_store_mode_gbs(uint64_t bytes, int reps, int mode, int warps_per_cta, int ctas_per_sm,
+                                 uint64_t slots);
 
 #ifdef __cplusplus
 }

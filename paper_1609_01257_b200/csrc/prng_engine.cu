@@ -1322,6 +1322,40 @@ double prng_probe_d2d_sweep_gbs(uint64_t chunk, uint64_t total, int reps) {
     return cudaGetLastError() == cudaSuccess ? best : -1;
 }
 
+double prng_probe_store_mode_gbs(uint64_t bytes, int reps, int mode, int warps_per_cta, int ctas_per_sm,
+                                 uint64_t slots) {
+    uint64_t *p = nullptr;
+    bytes &= ~15ull;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0;
+    uint64_t done = bytes;
+    for (int r = 0; r < reps + 1; ++r) {
+        cudaEventRecord(a);
+        prngk::store_pattern_kernel<<<sms * ctas_per_sm, 32 * warps_per_cta>>>(p, bytes / 16, mode,
+                                                                                 slots ? slots : 1);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (mode == 4) {  // bytes actually written: whole pieces only
+            const uint64_t cols = bytes / 16 / (slots ? slots : 1);
+            const uint64_t pw = 32ull * warps_per_cta * sms * ctas_per_sm;
+            done = (cols / pw) * pw * (slots ? slots : 1) * 16;
+        }
+        if (r) best = std::max(best, done / (ms * 1e-3) / 1e9);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(p);
+    return cudaGetLastError() == cudaSuccess ? best : -1;
+}
+
 double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams) {
     if (nstreams < 1) nstreams = 1;
     void *d = nullptr, *hbuf = nullptr;
