@@ -134,6 +134,7 @@ struct prng {
     uint64_t *d_ring = nullptr;
     uint64_t ring_pitch = 0, ring_slots = 0;
     uint64_t ring_cursor = 0;  // next slot to write; persists across prng_init (rotating ring)
+    bool ring_auto = false;    // the ring was sized automatically (PRNG_OPT_RING_SLOTS 0)
     uint64_t ring_iter0 = 0;   // slot holding iteration 0 of the current init
 
     // end-to-end buffers
@@ -691,6 +692,10 @@ static int ensure_ring(prng *h, uint64_t numiter, prng_err_t *err) {
     const uint64_t pitch = pitch_for(h->count) + (uint64_t)h->ring_pad;
     const uint64_t slot_bytes = pitch * sizeof(uint64_t);
     uint64_t slots = (uint64_t)h->ring_slots_opt;
+    // fast path: the ring exists and still matches the options (no cudaMemGetInfo, which
+    // costs milliseconds, on every generate call)
+    if (h->d_ring && h->ring_pitch == pitch && (slots == 0 ? h->ring_auto : slots == h->ring_slots))
+        return PRNG_OK;
     if (slots == 0) {
         uint64_t target = kRingBytes;
         size_t free_b = 0, total_b = 0;
@@ -701,7 +706,10 @@ static int ensure_ring(prng *h, uint64_t numiter, prng_err_t *err) {
         slots = std::max<uint64_t>(2, target / slot_bytes);
         slots = std::min<uint64_t>(slots, 0x7FFFFFFFull);
     }
-    if (h->d_ring && h->ring_slots == slots && h->ring_pitch == pitch) return PRNG_OK;
+    if (h->d_ring && h->ring_slots == slots && h->ring_pitch == pitch) {
+        h->ring_auto = h->ring_slots_opt == 0;
+        return PRNG_OK;
+    }
     if (h->d_ring) {
         CU(cudaStreamSynchronize(h->s_gen));
         cudaFree(h->d_ring);
@@ -710,6 +718,7 @@ static int ensure_ring(prng *h, uint64_t numiter, prng_err_t *err) {
     CU(cudaMalloc(&h->d_ring, slots * slot_bytes));
     h->ring_slots = slots;
     h->ring_pitch = pitch;
+    h->ring_auto = h->ring_slots_opt == 0;
     h->ring_cursor = 0;
     h->ring_iter0 = (slots - (h->pos % slots)) % slots;  // keep "iteration k -> (iter0 + k) mod R"
     (void)numiter;
