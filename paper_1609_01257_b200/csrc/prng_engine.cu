@@ -303,6 +303,8 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
                 h->jump_key[1] = L;
                 h->jump_key[2] = e;
             }
+            if (!h->d_state2)  // allocated on first use: small numrn only
+                CU(cudaMalloc(&h->d_state2, pitch_for(h->count) * sizeof(uint64_t)));
             a.nchunks = (uint32_t)C;
             a.chunk_len = (uint32_t)L;
             a.jump = h->d_jump;
@@ -451,8 +453,6 @@ prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begi
     }
     if ((e = cudaMalloc(&h->d_state, pitch_for(gid_count) * sizeof(uint64_t))) != cudaSuccess)
         return bail("cudaMalloc(state)", e);
-    if ((e = cudaMalloc(&h->d_state2, pitch_for(gid_count) * sizeof(uint64_t))) != cudaSuccess)
-        return bail("cudaMalloc(state2)", e);
     if ((e = cudaStreamCreateWithFlags(&h->s_gen, cudaStreamNonBlocking)) != cudaSuccess)
         return bail("cudaStreamCreate", e);
     if ((e = cudaStreamCreateWithFlags(&h->s_copy, cudaStreamNonBlocking)) != cudaSuccess)
