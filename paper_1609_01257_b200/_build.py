@@ -9,8 +9,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libprng_b200.so")
-SOURCES = [os.path.join(CSRC, "prng_engine.cu"), os.path.join(CSRC, "prng_prof.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, "prng_kernels.cuh"),
+SOURCES = [os.path.join(CSRC, f) for f in
+           ("prng_engine.cu", "prng_pipeline.cu", "prng_probes.cu", "prng_prof.cpp", "prng_sinks.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, "prng_kernels.cuh"), os.path.join(CSRC, "engine_internal.h"),
                   os.path.join(ROOT, "include", "prng.h"), os.path.join(ROOT, "include", "prng_sinks.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1,7 +1,7 @@
-// prng_engine.cu -- the C ABI of include/prng.h: handle lifecycle, kernel dispatch, the
-// device-only ring, the end-to-end pipeline (device double buffer + side copy stream +
-// pinned host double buffer + sink), interval capture for row a6, built-in sinks and the
-// roofline probes.
+// prng_engine.cu -- the C ABI of include/prng.h: handle lifecycle, options, kernel
+// variants and their launch (a1, a2 + a3), the device-only ring, checkpoint/seek,
+// autotune, interval capture (a6).  The end-to-end pipeline lives in prng_pipeline.cu,
+// the roofline probes in prng_probes.cu, the built-in sinks in prng_sinks.cpp.
 //
 // Paper mapping (§5):
 //   "main thread"  + Main queue  -> s_gen  (generation kernels)
@@ -9,13 +9,11 @@
 //   device-side double buffering -> two halves of a device ring of T-iteration batches
 //   semaphores between the threads -> CUDA events (gen(j) -> copy(j); copy(j) -> gen(j+2))
 //   limitation 2 (host-side dual buffer) -> two pinned host halves (mode O2)
-//   limitation 3 (no vectorisation) -> NPT numbers per thread, 32-byte stores
+//   limitation 3 (no vectorisation) -> NPT numbers per thread, vector stores
 #include <cuda_runtime.h>
 #include <sys/mman.h>
 
 #include <algorithm>
-#include <chrono>
-#include <cstdarg>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -24,40 +22,12 @@
 #include <string>
 #include <vector>
 
-#include "../../include/prng.h"
-#include "../../include/prng_sinks.h"
+#include "engine_internal.h"
 #include "prng_kernels.cuh"
 
-// ============================================================================ errors
+using namespace prng_detail;
+
 namespace {
-
-int set_err(prng_err_t *err, int code, const char *fmt, ...) {
-    if (err) {
-        err->code = code;
-        va_list ap;
-        va_start(ap, fmt);
-        std::vsnprintf(err->msg, sizeof(err->msg), fmt, ap);
-        va_end(ap);
-    }
-    return code;
-}
-int ok(prng_err_t *err) {
-    if (err) {
-        err->code = PRNG_OK;
-        err->msg[0] = 0;
-    }
-    return PRNG_OK;
-}
-
-#define CU(call)                                                                                    \
-    do {                                                                                            \
-        cudaError_t e_ = (call);                                                                    \
-        if (e_ != cudaSuccess) {                                                                    \
-            if (h) h->poisoned = true;                                                              \
-            return set_err(err, e_ == cudaErrorMemoryAllocation ? PRNG_ENOMEM : PRNG_ECUDA,        \
-                           "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);   \
-        }                                                                                           \
-    } while (0)
 
 // ============================================================================ kernel variants
 using BatchFn = void (*)(prngk::BatchArgs);
@@ -107,77 +77,13 @@ constexpr int kNumStar = sizeof(kStarFns) / sizeof(kStarFns[0]);
 size_t variant_smem(const Variant &v, uint64_t warps_per_block) {
     return v.stages ? (size_t)warps_per_block * v.stages * 32 * v.npt * sizeof(uint64_t) : 0;
 }
-constexpr int kBlock = 256;
-
-double now_s() {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
+static_assert(kNumVariants <= kMaxVariants, "raise kMaxVariants");
 
 }  // namespace
 
-// ============================================================================ the handle
-struct prng {
-    int device = 0;
-    int num_sms = 0;
-    int l2_bytes = 0;
-    uint64_t numrn_total = 0, seed = 0, gid_begin = 0, count = 0;
-    uint64_t pos = 0;  // iterations emitted since prng_init
-    bool inited = false, poisoned = false;
 
-    uint64_t *d_state = nullptr;   // [round_up(count, 4)]
-    uint64_t *d_state2 = nullptr;  // the other half of the state double buffer (time-parallel launches)
-    uint64_t *d_jump = nullptr;    // jump-ahead columns [chunks][64] (time-parallel launches)
-    uint64_t jump_cap = 0, jump_key[3] = {0, 0, 0};  // capacity (chunks), cached (C, L, e)
-    int time_parallel = 1;         // PRNG_OPT_TIME_PARALLEL
+namespace prng_detail {
 
-    // device-only ring
-    uint64_t *d_ring = nullptr;
-    uint64_t ring_pitch = 0, ring_slots = 0;
-    uint64_t ring_cursor = 0;  // next slot to write; persists across prng_init (rotating ring)
-    bool ring_auto = false;    // the ring was sized automatically (PRNG_OPT_RING_SLOTS 0)
-    uint64_t ring_iter0 = 0;   // slot holding iteration 0 of the current init
-
-    // end-to-end buffers
-    uint64_t *d_buf = nullptr;  // 2 halves x T slots, pitch buf_pitch
-    uint64_t buf_pitch = 0, buf_T = 0;
-    uint64_t *h_buf[2] = {nullptr, nullptr};
-    uint64_t *h_dev[2] = {nullptr, nullptr};  // device aliases of mapped host halves (zero-copy)
-    int h_kind = -1;                          // enum HostKind of the allocated halves
-    int host_mem = 0;                         // PRNG_OPT_HOST_MEM
-    uint64_t h_T = 0;
-    int h_halves = 0;
-
-    cudaStream_t s_gen = nullptr, s_copy = nullptr;
-    bool own_streams = true;
-
-    // options
-    int mode = PRNG_MODE_OVERLAP2;
-    int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0, ring_pad = 0, cta_warps = 0;
-    unsigned long long *trace = nullptr;  // PRNG_OPT_TRACE_PTR (diagnostic variant only)
-
-    int profile = 0, kernel = 0, output = 0, blocking = 1;
-    int blocks_per_sm[kNumVariants] = {0};
-
-    // profiling (a6)
-    cudaEvent_t ev_origin = nullptr;
-    double host_origin = 0;
-    struct DevIv {
-        uint32_t name;
-        cudaEvent_t a, b;
-    };
-    std::vector<DevIv> dev_iv;
-    struct HostIv {
-        uint32_t name;
-        double a, b;
-    };
-    std::vector<HostIv> host_iv;
-    double wall_s = 0;
-};
-
-namespace {
-
-// Host buffer kinds (PRNG_OPT_HOST_MEM selects among the pinned ones).
-enum HostKind { HK_PINNED = 0, HK_PINNED_WC = 1, HK_HUGE_REGISTERED = 2, HK_MAPPED = 3, HK_PAGEABLE = 4 };
 
 void free_host(int kind, void *p, size_t bytes) {
     if (!p) return;
@@ -193,7 +99,6 @@ void free_host(int kind, void *p, size_t bytes) {
     }
 }
 
-uint64_t pitch_for(uint64_t count) { return (count + 3) & ~3ull; }  // 32-byte aligned slots
 
 void free_e2e(prng *h) {
     if (h->d_buf) cudaFree(h->d_buf);
@@ -368,7 +273,7 @@ int check_handle(prng *h, prng_err_t *err, bool need_init) {
     return PRNG_OK;
 }
 
-}  // namespace
+}  // namespace prng_detail
 
 // ============================================================================ C ABI
 extern "C" {
@@ -815,338 +720,12 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
     return ok(err);
 }
 
-// ---------------------------------------------------------------------------- end to end
-// Device double buffer of the end-to-end paths: 2 halves x T slots.
-static int ensure_dbuf(prng *h, uint64_t T, prng_err_t *err) {
-    const uint64_t pitch = pitch_for(h->count);
-    if (!h->d_buf || h->buf_T != T || h->buf_pitch != pitch) {
-        if (h->d_buf) cudaFree(h->d_buf);
-        h->d_buf = nullptr;
-        CU(cudaMalloc(&h->d_buf, 2 * T * pitch * sizeof(uint64_t)));
-        h->buf_T = T;
-        h->buf_pitch = pitch;
-    }
-    return PRNG_OK;
-}
-
-static int ensure_e2e(prng *h, uint64_t T, int halves, int kind, bool need_dbuf, prng_err_t *err) {
-    if (need_dbuf)
-        if (int rc = ensure_dbuf(h, T, err)) return rc;
-    if (h->h_T != T || h->h_halves < halves || h->h_kind != kind) {
-        for (int i = 0; i < 2; ++i) {
-            free_host(h->h_kind, h->h_buf[i], h->h_T * h->count * sizeof(uint64_t));
-            h->h_buf[i] = h->h_dev[i] = nullptr;
-        }
-        h->h_kind = kind;
-        h->h_T = T;
-        h->h_halves = 0;
-        const size_t bytes = T * h->count * sizeof(uint64_t);
-        for (int i = 0; i < halves; ++i) {
-            void *p = nullptr;
-            switch (kind) {
-                case HK_PINNED: CU(cudaHostAlloc(&p, bytes, cudaHostAllocDefault)); break;
-                case HK_PINNED_WC: CU(cudaHostAlloc(&p, bytes, cudaHostAllocWriteCombined)); break;
-                case HK_MAPPED: CU(cudaHostAlloc(&p, bytes, cudaHostAllocMapped)); break;
-                case HK_HUGE_REGISTERED: {
-                    // anonymous mapping advised onto 2 MiB transparent huge pages, then pinned
-                    p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
-                    if (p == MAP_FAILED) return set_err(err, PRNG_ENOMEM, "mmap(%zu)", bytes);
-                    madvise(p, bytes, MADV_HUGEPAGE);
-                    std::memset(p, 0, bytes);
-                    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterDefault);
-                    if (e != cudaSuccess) {
-                        munmap(p, bytes);
-                        return set_err(err, PRNG_ECUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
-                    }
-                    break;
-                }
-                default:
-                    p = std::malloc(bytes);
-                    if (!p) return set_err(err, PRNG_ENOMEM, "malloc(%zu)", bytes);
-            }
-            h->h_buf[i] = (uint64_t *)p;
-            if (kind == HK_MAPPED) CU(cudaHostGetDevicePointer((void **)&h->h_dev[i], p, 0));
-            h->h_halves = i + 1;
-        }
-    }
-    return PRNG_OK;
-}
-
-// O3 (zero-copy): the generation kernel stores each batch straight into a mapped pinned
-// host half over PCIe -- no device ring, no copy engine; the store IS the transfer.
-// sink(j) runs while gen(j+1) writes the other half; gen(j+2) is enqueued after sink(j).
-static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, uint64_t T_alloc, prng_sink_fn sink,
-                             void *user, prng_err_t *err) {
-    if (h->count % 4) return set_err(err, PRNG_EINVAL, "zero-copy mode needs count %% 4 == 0 (32-B aligned rows)");
-    if (int rc = ensure_e2e(h, T_alloc, 2, HK_MAPPED, false, err)) return rc;
-    const double t0 = now_s();  // wall time of the profiled call, allocations excluded
-    const uint64_t nb = (numiter + T - 1) / T;
-    const uint64_t pos0 = h->pos;
-    auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    for (auto &e : ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    int rc = PRNG_OK;
-    auto gen = [&](uint64_t j) -> int {
-        if (int r = launch_batch(h, h->h_dev[j & 1], h->count, T, 0, iters_of(j), pos0 + j * T == 0, h->s_gen, err))
-            return r;
-        cudaError_t e = cudaEventRecord(ev[j & 1], h->s_gen);
-        return e == cudaSuccess ? PRNG_OK : set_err(err, PRNG_ECUDA, "cudaEventRecord: %s", cudaGetErrorString(e));
-    };
-    for (uint64_t j = 0; j < std::min<uint64_t>(nb, 2) && !rc; ++j) rc = gen(j);
-    for (uint64_t j = 0; j < nb && !rc; ++j) {
-        cudaError_t e = cudaEventSynchronize(ev[j & 1]);
-        if (e != cudaSuccess) {
-            rc = set_err(err, PRNG_ECUDA, "cudaEventSynchronize: %s", cudaGetErrorString(e));
-            break;
-        }
-        const double a = now_s();
-        int r = sink(user, pos0 + j * T, iters_of(j), h->gid_begin, h->count, h->h_buf[j & 1]);
-        if (h->profile) h->host_iv.push_back({PRNG_EV_OUT, a - h->host_origin, now_s() - h->host_origin});
-        if (r != 0) {
-            rc = set_err(err, PRNG_ESINK, "sink returned %d at batch %llu", r, (unsigned long long)j);
-            break;
-        }
-        if (j + 2 < nb) rc = gen(j + 2);
-    }
-    cudaStreamSynchronize(h->s_gen);
-    for (auto &e : ev) cudaEventDestroy(e);
-    if (rc) {
-        h->poisoned = true;
-        return rc;
-    }
-    h->pos = pos0 + numiter;
-    h->wall_s += now_s() - t0;
-    return PRNG_OK;
-}
-
-static int enqueue_copy(prng *h, uint64_t *hdst, const uint64_t *dsrc, uint64_t iters, cudaStream_t s,
-                        prng_err_t *err) {
-    if (int rc = prof_begin(h, s, PRNG_EV_READ_BUFFER, err)) return rc;
-    const size_t row = h->count * sizeof(uint64_t);
-    if (h->buf_pitch == h->count) {
-        CU(cudaMemcpyAsync(hdst, dsrc, row * iters, cudaMemcpyDeviceToHost, s));
-    } else {
-        CU(cudaMemcpy2DAsync(hdst, row, dsrc, h->buf_pitch * sizeof(uint64_t), row, iters, cudaMemcpyDeviceToHost, s));
-    }
-    return prof_end(h, s, err);
-}
-
-static int generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void *user, prng_err_t *err) {
-    uint64_t T = (uint64_t)h->batch_iters;
-    const uint64_t row = h->count * sizeof(uint64_t);
-    if (T == 0) T = std::max<uint64_t>(1, (256ull << 20) / row);  // ~256 MiB per batch
-    const uint64_t T_alloc = T;  // buffers are sized for full batches: no re-allocation per call
-    T = std::min<uint64_t>(T, numiter);
-    const int mode = h->mode;
-    if (mode == PRNG_MODE_ZEROCOPY) {
-        return generate_zerocopy(h, numiter, T, T_alloc, sink, user, err);
-    }
-    const int halves = (mode == PRNG_MODE_OVERLAP2 || mode == PRNG_MODE_PAGEABLE) ? 2 : 1;
-    if (int rc = ensure_e2e(h, T_alloc, halves, mode == PRNG_MODE_PAGEABLE ? HK_PAGEABLE : h->host_mem, true, err))
-        return rc;
-    const uint64_t nb = (numiter + T - 1) / T;
-    const uint64_t pitch = h->buf_pitch;
-    auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
-    auto dslot = [&](uint64_t j) { return (mode == PRNG_MODE_SERIAL ? 0 : (j & 1)) * T; };
-    const uint64_t pos0 = h->pos;
-    const double t0 = now_s();
-
-    auto run_sink = [&](uint64_t j, const uint64_t *data) -> int {
-        const double a = now_s();
-        int r = sink ? sink(user, pos0 + j * T, iters_of(j), h->gid_begin, h->count, data) : 0;
-        if (h->profile) h->host_iv.push_back({PRNG_EV_OUT, a - h->host_origin, now_s() - h->host_origin});
-        if (r != 0) {
-            h->poisoned = true;
-            return set_err(err, PRNG_ESINK, "sink returned %d at batch %llu", r, (unsigned long long)j);
-        }
-        return PRNG_OK;
-    };
-
-    if (mode == PRNG_MODE_SERIAL) {
-        // S0: everything on one stream, one buffer each side: gen -> read -> out -> gen ...
-        for (uint64_t j = 0; j < nb; ++j) {
-            if (int rc = launch_batch(h, h->d_buf, pitch, 2 * T, 0, iters_of(j), pos0 + j * T == 0, h->s_gen, err))
-                return rc;
-            if (int rc = enqueue_copy(h, h->h_buf[0], h->d_buf, iters_of(j), h->s_gen, err)) return rc;
-            CU(cudaStreamSynchronize(h->s_gen));
-            if (int rc = run_sink(j, h->h_buf[0])) return rc;
-        }
-        h->pos = pos0 + numiter;
-        h->wall_s += now_s() - t0;
-        return PRNG_OK;
-    }
-
-    // Overlapped modes (S1, O1, O2): gen stream + copy stream + events.
-    const int R = 8;  // event ring; at most gen(j+4) / copy(j+2) ahead of the host at batch j
-    cudaEvent_t ev_gen[R], ev_cp[R];
-    for (int i = 0; i < R; ++i) {
-        ev_gen[i] = ev_cp[i] = nullptr;
-    }
-    int rc = PRNG_OK;
-    auto cleanup = [&]() {
-        for (int i = 0; i < R; ++i) {
-            if (ev_gen[i]) cudaEventDestroy(ev_gen[i]);
-            if (ev_cp[i]) cudaEventDestroy(ev_cp[i]);
-        }
-    };
-    for (int i = 0; i < R; ++i) {
-        cudaError_t e1 = cudaEventCreateWithFlags(&ev_gen[i], cudaEventDisableTiming);
-        cudaError_t e2 = cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming);
-        if (e1 != cudaSuccess || e2 != cudaSuccess) {
-            cleanup();
-            h->poisoned = true;
-            return set_err(err, PRNG_ECUDA, "cudaEventCreate failed");
-        }
-    }
-    uint64_t gen_enq = 0, cp_enq = 0;  // batches enqueued so far
-    auto enqueue_gen = [&](uint64_t j) -> int {
-        // gen(j) overwrites device half j%2, last read by copy(j-2)  (WAR, A15)
-        if (j >= 2) {
-            cudaError_t e = cudaStreamWaitEvent(h->s_gen, ev_cp[(j - 2) % R], 0);
-            if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
-        }
-        if (int r = launch_batch(h, h->d_buf, pitch, 2 * T, dslot(j), iters_of(j), pos0 + j * T == 0, h->s_gen, err))
-            return r;
-        cudaError_t e = cudaEventRecord(ev_gen[j % R], h->s_gen);
-        if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaEventRecord: %s", cudaGetErrorString(e));
-        gen_enq = j + 1;
-        return PRNG_OK;
-    };
-    auto enqueue_cp = [&](uint64_t j) -> int {
-        // copy(j) reads device half j%2 after gen(j) wrote it  (RAW, A15)
-        cudaError_t e = cudaStreamWaitEvent(h->s_copy, ev_gen[j % R], 0);
-        if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
-        if (int r = enqueue_copy(h, h->h_buf[j % halves], h->d_buf + dslot(j) * pitch, iters_of(j), h->s_copy, err))
-            return r;
-        e = cudaEventRecord(ev_cp[j % R], h->s_copy);
-        if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "cudaEventRecord: %s", cudaGetErrorString(e));
-        cp_enq = j + 1;
-        return PRNG_OK;
-    };
-
-    // Prologue: gen(0), copy(0), gen(1), [copy(1) if a second host half], gen(2), gen(3).
-    for (uint64_t j = 0; j < std::min<uint64_t>(nb, 2) && !rc; ++j) {
-        rc = enqueue_gen(j);
-        if (!rc && j < (uint64_t)halves) rc = enqueue_cp(j);
-    }
-    while (!rc && gen_enq < nb && gen_enq < cp_enq + 2) rc = enqueue_gen(gen_enq);
-
-    for (uint64_t j = 0; j < nb && !rc; ++j) {
-        cudaError_t e = cudaEventSynchronize(ev_cp[j % R]);
-        if (e != cudaSuccess) {
-            rc = set_err(err, PRNG_ECUDA, "cudaEventSynchronize: %s", cudaGetErrorString(e));
-            break;
-        }
-        rc = run_sink(j, h->h_buf[j % halves]);
-        if (rc) break;
-        // host half j%halves is free again: queue the next copy into it, then the next gen
-        if (cp_enq < nb) rc = enqueue_cp(cp_enq);
-        while (!rc && gen_enq < nb && gen_enq < cp_enq + 2) rc = enqueue_gen(gen_enq);
-    }
-    if (rc) {
-        cudaStreamSynchronize(h->s_gen);
-        cudaStreamSynchronize(h->s_copy);
-        cleanup();
-        h->poisoned = true;
-        return rc;
-    }
-    cudaStreamSynchronize(h->s_gen);
-    cleanup();
-    h->pos = pos0 + numiter;
-    h->wall_s += now_s() - t0;
-    return PRNG_OK;
-}
-
 int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, prng_err_t *err) {
     if (int rc = check_handle(h, err, true)) return rc;
     if (numiter < 1) return set_err(err, PRNG_EINVAL, "numiter must be >= 1");
     if (int rc = ensure_origin(h, err)) return rc;
     int rc = sink ? generate_e2e(h, numiter, sink, user, err) : generate_device_only(h, numiter, err);
     if (rc) return rc;
-    return ok(err);
-}
-
-// ---------------------------------------------------------------------------- host array
-// a4 + a5, multi-rank form (BASELINE north_star: "each rank generates its own gid range and
-// writes its slice of the host output directly"): D2H straight into the caller's host array
-// -- no staging buffer, no sink.  Iteration k of this call lands in row k mod dst_rows:
-// dst[(k mod dst_rows) * dst_pitch + j], j < count.  For a shared array the caller passes
-// dst = array + gid_begin and dst_pitch = numrn_total, so every rank fills its own columns.
-int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch, uint64_t dst_rows,
-                       prng_err_t *err) {
-    if (int rc = check_handle(h, err, true)) return rc;
-    if (numiter < 1 || !dst || dst_pitch < h->count || dst_rows < 1)
-        return set_err(err, PRNG_EINVAL, "numiter >= 1, dst != NULL, dst_pitch >= count, dst_rows >= 1");
-    if (int rc = ensure_origin(h, err)) return rc;
-    const uint64_t row = h->count * sizeof(uint64_t);
-    uint64_t T = (uint64_t)h->batch_iters;
-    if (T == 0) T = std::max<uint64_t>(1, (256ull << 20) / row);
-    if (int rc = ensure_dbuf(h, T, err)) return rc;
-    T = std::min<uint64_t>(T, numiter);
-    // pin the destination for the DMA engine unless it already is (registered / cudaHostAlloc)
-    const size_t span = ((std::min<uint64_t>(dst_rows, numiter) - 1) * dst_pitch + h->count) * sizeof(uint64_t);
-    cudaPointerAttributes attr;
-    bool registered_here = false;
-    if (cudaPointerGetAttributes(&attr, dst) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
-        cudaGetLastError();
-        CU(cudaHostRegister(dst, span, cudaHostRegisterDefault));
-        registered_here = true;
-    }
-    const uint64_t nb = (numiter + T - 1) / T, pitch = h->buf_pitch, pos0 = h->pos;
-    auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
-    const int R = 4;
-    cudaEvent_t ev_gen[R], ev_cp[R];
-    for (int i = 0; i < R; ++i) {
-        cudaEventCreateWithFlags(&ev_gen[i], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming);
-    }
-    int rc = PRNG_OK;
-    const double t0 = now_s();
-    for (uint64_t j = 0; j < nb && !rc; ++j) {
-        // gen(j) into device half j%2, after copy(j-2) has drained it (WAR, A15)
-        if (j >= 2 && cudaStreamWaitEvent(h->s_gen, ev_cp[(j - 2) % R], 0) != cudaSuccess) {
-            rc = set_err(err, PRNG_ECUDA, "cudaStreamWaitEvent");
-            break;
-        }
-        rc = launch_batch(h, h->d_buf, pitch, 2 * T, (j & 1) * T, iters_of(j), pos0 + j * T == 0, h->s_gen, err);
-        if (rc) break;
-        cudaEventRecord(ev_gen[j % R], h->s_gen);
-        // copy(j): rows (pos0 + j*T + t) mod dst_rows, split where the host ring wraps
-        cudaStreamWaitEvent(h->s_copy, ev_gen[j % R], 0);
-        if ((rc = prof_begin(h, h->s_copy, PRNG_EV_READ_BUFFER, err))) break;
-        uint64_t t = 0;
-        while (t < iters_of(j)) {
-            const uint64_t r0 = (j * T + t) % dst_rows;  // destination row of call iteration j*T + t
-            const uint64_t nrows = std::min<uint64_t>(iters_of(j) - t, dst_rows - r0);
-            const cudaError_t e = cudaMemcpy2DAsync(dst + r0 * dst_pitch, dst_pitch * sizeof(uint64_t),
-                                                    h->d_buf + ((j & 1) * T + t) * pitch, pitch * sizeof(uint64_t), row,
-                                                    nrows, cudaMemcpyDeviceToHost, h->s_copy);
-            if (e != cudaSuccess) {
-                rc = set_err(err, PRNG_ECUDA, "cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
-                break;
-            }
-            t += nrows;
-        }
-        if (rc) break;
-        if ((rc = prof_end(h, h->s_copy, err))) break;
-        cudaEventRecord(ev_cp[j % R], h->s_copy);
-        // keep at most two batches in flight per stream (the event ring has R = 4 entries)
-        if (j >= 2) cudaEventSynchronize(ev_cp[(j - 2) % R]);
-    }
-    cudaStreamSynchronize(h->s_gen);
-    const cudaError_t e = cudaStreamSynchronize(h->s_copy);
-    for (int i = 0; i < R; ++i) {
-        cudaEventDestroy(ev_gen[i]);
-        cudaEventDestroy(ev_cp[i]);
-    }
-    if (registered_here) cudaHostUnregister(dst);
-    if (!rc && e != cudaSuccess) rc = set_err(err, PRNG_ECUDA, "copy stream: %s", cudaGetErrorString(e));
-    if (rc) {
-        h->poisoned = true;
-        return rc;
-    }
-    h->pos = pos0 + numiter;
-    h->wall_s += now_s() - t0;
     return ok(err);
 }
 
@@ -1208,203 +787,6 @@ int prng_prof_events(const prng_t *hc, uint64_t cap, uint32_t *name_id, double *
         ++i;
     }
     return ok(err);
-}
-
-// ---------------------------------------------------------------------------- built-in sinks
-int prng_sink_null(void *, uint64_t, uint32_t, uint64_t, uint64_t, const uint64_t *) { return 0; }
-
-int prng_sink_copy(void *user, uint64_t iter_begin, uint32_t iters, uint64_t gid_begin, uint64_t count,
-                   const uint64_t *data) {
-    prng_copy_sink_t *c = (prng_copy_sink_t *)user;
-    for (uint32_t t = 0; t < iters; ++t) {
-        const uint64_t k = iter_begin + t;
-        if (k < c->iter_offset || k - c->iter_offset >= c->iters) return 1;
-        std::memcpy(c->dst + (k - c->iter_offset) * c->dst_pitch + (gid_begin - c->gid_offset), data + t * count,
-                    count * sizeof(uint64_t));
-    }
-    return 0;
-}
-
-int prng_sink_digest(void *user, uint64_t iter_begin, uint32_t iters, uint64_t, uint64_t count,
-                     const uint64_t *data) {
-    prng_digest_sink_t *d = (prng_digest_sink_t *)user;
-    for (uint32_t t = 0; t < iters; ++t) {
-        const uint64_t k = iter_begin + t;
-        if (k < d->iter_offset || k - d->iter_offset >= d->iters) return 1;
-        uint64_t x = 0, s = 0;
-        const uint64_t *row = data + (uint64_t)t * count;
-        for (uint64_t j = 0; j < count; ++j) {
-            x ^= row[j];
-            s += row[j];
-        }
-        d->xor_out[k - d->iter_offset] ^= x;
-        d->sum_out[k - d->iter_offset] += s;
-    }
-    return 0;
-}
-
-// ---------------------------------------------------------------------------- probes
-double prng_probe_memset_gbs(uint64_t bytes, int reps) {
-    void *p = nullptr;
-    if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    double best = 0;
-    cudaMemset(p, 1, bytes);
-    for (int r = 0; r < reps; ++r) {
-        cudaEventRecord(a);
-        cudaMemsetAsync(p, r & 0xff, bytes);
-        cudaEventRecord(b);
-        cudaEventSynchronize(b);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, a, b);
-        best = std::max(best, bytes / (ms * 1e-3) / 1e9);
-    }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    cudaFree(p);
-    return cudaGetLastError() == cudaSuccess ? best : -1;
-}
-
-double prng_probe_store_gbs(uint64_t bytes, int reps) { return prng_probe_store_pattern_gbs(bytes, reps, 0, 0); }
-
-double prng_probe_store_pattern_gbs(uint64_t bytes, int reps, int pattern, int warps_per_sm) {
-    uint64_t *p = nullptr;
-    bytes &= ~31ull;
-    if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
-    int dev = 0, sms = 0, bps = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, prngk::store_probe_kernel, kBlock, 0);
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    double best = 0;
-    for (int r = 0; r < reps + 1; ++r) {
-        cudaEventRecord(a);
-        if (warps_per_sm > 0)
-            prngk::store_probe_kernel<<<sms, 32 * std::min(warps_per_sm, 32), 0>>>(p, bytes / 32, pattern);
-        else
-            prngk::store_probe_kernel<<<sms * std::max(bps, 1), kBlock>>>(p, bytes / 32, pattern);
-        cudaEventRecord(b);
-        cudaEventSynchronize(b);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, a, b);
-        if (r) best = std::max(best, bytes / (ms * 1e-3) / 1e9);
-    }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    cudaFree(p);
-    return cudaGetLastError() == cudaSuccess ? best : -1;
-}
-
-// Copy-engine write probe: a `chunk`-byte (L2-resident) source copied D2D over a `total`-byte
-// destination, chunk by chunk (cudaMemcpyAsync), i.e. the DRAM sees a sequential write
-// sweep fed from L2.  Returns destination GB/s (best of reps).
-double prng_probe_d2d_sweep_gbs(uint64_t chunk, uint64_t total, int reps) {
-    void *src = nullptr, *dst = nullptr;
-    if (cudaMalloc(&src, chunk) != cudaSuccess) return -1;
-    if (cudaMalloc(&dst, total) != cudaSuccess) {
-        cudaFree(src);
-        return -1;
-    }
-    cudaMemset(src, 3, chunk);
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    double best = 0;
-    for (int r = 0; r < reps + 1; ++r) {
-        cudaEventRecord(a);
-        for (uint64_t off = 0; off + chunk <= total; off += chunk)
-            cudaMemcpyAsync((char *)dst + off, src, chunk, cudaMemcpyDeviceToDevice);
-        cudaEventRecord(b);
-        cudaEventSynchronize(b);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, a, b);
-        if (r) best = std::max(best, (total / chunk) * (double)chunk / (ms * 1e-3) / 1e9);
-    }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    cudaFree(src);
-    cudaFree(dst);
-    return cudaGetLastError() == cudaSuccess ? best : -1;
-}
-
-double prng_probe_store_mode_gbs(uint64_t bytes, int reps, int mode, int warps_per_cta, int ctas_per_sm,
-                                 uint64_t slots) {
-    uint64_t *p = nullptr;
-    bytes &= ~15ull;
-    if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    double best = 0;
-    uint64_t done = bytes;
-    for (int r = 0; r < reps + 1; ++r) {
-        cudaEventRecord(a);
-        prngk::store_pattern_kernel<<<sms * ctas_per_sm, 32 * warps_per_cta>>>(p, bytes / 16, mode,
-                                                                                 slots ? slots : 1);
-        cudaEventRecord(b);
-        cudaEventSynchronize(b);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, a, b);
-        if (mode == 4) {  // bytes actually written: whole pieces only
-            const uint64_t cols = bytes / 16 / (slots ? slots : 1);
-            const uint64_t pw = 32ull * warps_per_cta * sms * ctas_per_sm;
-            done = (cols / pw) * pw * (slots ? slots : 1) * 16;
-        }
-        if (r) best = std::max(best, done / (ms * 1e-3) / 1e9);
-    }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    cudaFree(p);
-    return cudaGetLastError() == cudaSuccess ? best : -1;
-}
-
-double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams) {
-    if (nstreams < 1) nstreams = 1;
-    void *d = nullptr, *hbuf = nullptr;
-    if (cudaMalloc(&d, bytes) != cudaSuccess) return -1;
-    cudaMemset(d, 7, bytes);
-    if (pinned) {
-        if (cudaHostAlloc(&hbuf, bytes, cudaHostAllocDefault) != cudaSuccess) {
-            cudaFree(d);
-            return -1;
-        }
-    } else {
-        hbuf = std::malloc(bytes);
-        if (!hbuf) {
-            cudaFree(d);
-            return -1;
-        }
-        std::memset(hbuf, 0, bytes);
-    }
-    std::vector<cudaStream_t> ss(nstreams);
-    for (auto &s : ss) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    double best = 0;
-    const uint64_t chunk = (bytes / nstreams) & ~4095ull;
-    for (int r = 0; r < reps + 1; ++r) {
-        cudaDeviceSynchronize();
-        const double t0 = now_s();
-        for (int i = 0; i < nstreams; ++i) {
-            const uint64_t off = i * chunk, len = (i == nstreams - 1) ? bytes - off : chunk;
-            cudaMemcpyAsync((char *)hbuf + off, (char *)d + off, len, cudaMemcpyDeviceToHost, ss[i]);
-        }
-        for (auto &s : ss) cudaStreamSynchronize(s);
-        const double dt = now_s() - t0;
-        if (r) best = std::max(best, bytes / dt / 1e9);
-    }
-    for (auto &s : ss) cudaStreamDestroy(s);
-    if (pinned)
-        cudaFreeHost(hbuf);
-    else
-        std::free(hbuf);
-    cudaFree(d);
-    return cudaGetLastError() == cudaSuccess ? best : -1;
 }
 
 }  // extern "C"

@@ -513,68 +513,4 @@ __global__ void __launch_bounds__(256) batch_kernel_tma(BatchArgs a) {
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// ---------------------------------------------------------------- roofline probe kernel
-// Pure 32-byte grid-stride store stream: the same-box SM write ceiling.  pattern 0: the
-// index (i, i+1, ...), 1: zeros, 2: pseudo-random (xorshift64 of the index) -- to see
-// whether the data values change the write rate (e.g. compression of constant data).
-__global__ void __launch_bounds__(256) store_probe_kernel(uint64_t *p, uint64_t n4, int pattern) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
-        if (pattern == 1) {
-            st_v4<0>(p + 4 * i, 0, 0, 0, 0);
-        } else if (pattern == 2) {
-            const uint64_t x = xorshift64(i * 0x9E3779B97F4A7C15ull + 1);
-            st_v4<0>(p + 4 * i, x, x ^ 0xA5A5A5A5A5A5A5A5ull, x * 3, ~x);
-        } else {
-            st_v4<0>(p + 4 * i, i, i + 1, i + 2, i + 3);
-        }
-    }
-}
-
-
-// Store-pattern microbenchmark (research probe, not on the path): 16-byte stores.
-//   mode 0: grid-stride sweep (consecutive warps adjacent, the grid sweeps forward)
-//   mode 1: mode 0 + a CTA barrier after every warp-store round
-//   mode 2: blocked -- CTA b sweeps its own contiguous 1/gridDim of the buffer
-//   mode 3: mode 2 + a CTA barrier after every round
-//   mode 4: "slot-strided" like the generator: the buffer is `slots` rows; each round a
-//           CTA writes its 4 KiB-ish chunk in row r mod slots, advancing one row per round
-__global__ void __launch_bounds__(256) store_pattern_kernel(uint64_t *p, uint64_t n2, int mode, uint64_t slots) {
-    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-    if (mode <= 1) {
-        for (uint64_t i = tid; i < n2; i += nthreads) {
-            st_v2<0>(p + 2 * i, i, ~i);
-            if (mode == 1) __syncthreads();
-        }
-    } else if (mode >= 100) {
-        // mode 100 + k: grid-stride with k dependent xorshift steps between stores (pacing)
-        uint64_t x = tid + 1;
-        for (uint64_t i = tid; i < n2; i += nthreads) {
-            for (int j = 0; j < mode - 100; ++j) x = xorshift64(x);
-            st_v2<0>(p + 2 * i, i, x);
-        }
-    } else if (mode <= 3) {
-        const uint64_t per = (n2 + gridDim.x - 1) / gridDim.x;
-        const uint64_t b0 = blockIdx.x * per, b1 = b0 + per < n2 ? b0 + per : n2;
-        for (uint64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-            st_v2<0>(p + 2 * i, i, ~i);
-            if (mode == 3) __syncthreads();
-        }
-    } else {
-        // row-major [slots][cols]: CTA b owns columns [b*blockDim, (b+1)*blockDim) of a
-        // "piece" and walks rows; pieces advance after `slots` rows (like the generator).
-        const uint64_t cols = n2 / slots;  // vec2 elements per row
-        const uint64_t piece_w = blockDim.x;
-        const uint64_t npieces = cols / (piece_w * gridDim.x);
-        for (uint64_t pc = 0; pc < npieces; ++pc) {
-            const uint64_t col = (pc * gridDim.x + blockIdx.x) * piece_w + threadIdx.x;
-            for (uint64_t r = 0; r < slots; ++r) {
-                st_v2<0>(p + 2 * (r * cols + col), r, col);
-                __syncthreads();
-            }
-        }
-    }
-}
-
 }  // namespace prngk

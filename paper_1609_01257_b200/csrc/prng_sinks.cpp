@@ -1,0 +1,42 @@
+// prng_sinks.cpp -- the built-in sinks of include/prng_sinks.h (the paper's `out`).
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/prng_sinks.h"
+
+extern "C" {
+
+// ---------------------------------------------------------------------------- built-in sinks
+int prng_sink_null(void *, uint64_t, uint32_t, uint64_t, uint64_t, const uint64_t *) { return 0; }
+
+int prng_sink_copy(void *user, uint64_t iter_begin, uint32_t iters, uint64_t gid_begin, uint64_t count,
+                   const uint64_t *data) {
+    prng_copy_sink_t *c = (prng_copy_sink_t *)user;
+    for (uint32_t t = 0; t < iters; ++t) {
+        const uint64_t k = iter_begin + t;
+        if (k < c->iter_offset || k - c->iter_offset >= c->iters) return 1;
+        std::memcpy(c->dst + (k - c->iter_offset) * c->dst_pitch + (gid_begin - c->gid_offset), data + t * count,
+                    count * sizeof(uint64_t));
+    }
+    return 0;
+}
+
+int prng_sink_digest(void *user, uint64_t iter_begin, uint32_t iters, uint64_t, uint64_t count,
+                     const uint64_t *data) {
+    prng_digest_sink_t *d = (prng_digest_sink_t *)user;
+    for (uint32_t t = 0; t < iters; ++t) {
+        const uint64_t k = iter_begin + t;
+        if (k < d->iter_offset || k - d->iter_offset >= d->iters) return 1;
+        uint64_t x = 0, s = 0;
+        const uint64_t *row = data + (uint64_t)t * count;
+        for (uint64_t j = 0; j < count; ++j) {
+            x ^= row[j];
+            s += row[j];
+        }
+        d->xor_out[k - d->iter_offset] ^= x;
+        d->sum_out[k - d->iter_offset] += s;
+    }
+    return 0;
+}
+
+}  // extern "C"
