@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--kernel", type=int, default=0, help="kernel variant id (default 0 = v2n4s1; -1: prng_autotune)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1)
-    ap.add_argument("--e2e-mode", type=int, default=3, help="0 S0, 1 S1, 2 O1, 3 O2")
+    ap.add_argument("--e2e-mode", type=int, default=3, help="0 S0, 1 S1, 2 O1, 3 O2, 4 O3 (zero-copy)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probes", action="store_true")
@@ -367,7 +367,7 @@ def run_ours(a, D):
         d2h_gbs = 8 * cnt * a.numiter * a.e2e_steps / sum(walls) / 1e9
         e2e = {"value": ev, "unit": "numbers/s", "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": 8 * numrn * a.numiter, "gbs": 8 * ev / 1e9,
-               "mode": ["S0", "S1", "O1", "O2"][a.e2e_mode], "d2h_gbs_per_gpu": d2h_gbs,
+               "mode": ["S0", "S1", "O1", "O2", "O3"][a.e2e_mode], "d2h_gbs_per_gpu": d2h_gbs,
                "profile_extra_step": {
                    "rng_kernel_s": agg[1], "read_buffer_s": agg[2], "out_s": agg[3], "init_s": agg[0],
                    "rng_read_overlap_s": ov[1, 2],
