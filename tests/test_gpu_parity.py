@@ -669,3 +669,31 @@ def test_seek_far_ahead():
         for t in range(m):
             x = oracle.xorshift64(x)
             assert int(out[t, g]) == x
+
+
+def test_argument_errors_on_a_live_handle():
+    """EINVAL paths that need a handle: option values, device-buffer layout, host array."""
+    import torch
+    h = P.prng_create(1000, 0)
+    try:
+        for opt, bad in [(P.PRNG_OPT_MODE, 9), (P.PRNG_OPT_KERNEL, 999), (P.PRNG_OPT_OUTPUT, 2),
+                         (P.PRNG_OPT_RING_PAD, 3), (P.PRNG_OPT_HOST_MEM, 7), (P.PRNG_OPT_PROFILE, 5),
+                         (P.PRNG_OPT_CTA_WARPS, 9), (99, 0)]:
+            with pytest.raises(P.PrngError) as e:
+                P.prng_set_option(h, opt, bad)
+            assert e.value.code == P.PRNG_EINVAL, (opt, bad)
+        P.prng_init(h)
+        buf = torch.zeros(8 * 1024 + 8, dtype=torch.int64, device="cuda")
+        for ptr, pitch in [(buf.data_ptr() + 8, 1000), (buf.data_ptr(), 1001), (buf.data_ptr(), 996)]:
+            with pytest.raises(P.PrngError) as e:
+                P.prng_generate_device(h, 2, ptr, pitch, 2)
+            assert e.value.code == P.PRNG_EINVAL
+        arr = np.zeros((2, 1000), np.uint64)
+        with pytest.raises(P.PrngError):
+            P.prng_generate_host(h, 0, arr, 1000, 2)
+        with pytest.raises(P.PrngError):
+            P.prng_generate_host(h, 2, arr, 999, 2)
+        P.prng_generate_host(h, 2, arr, 1000, 2)    # still usable after rejected calls
+        assert np.array_equal(arr, oracle.stream(1000, 2, 0))
+    finally:
+        P.prng_destroy(h)
