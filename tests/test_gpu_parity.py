@@ -697,3 +697,41 @@ def test_argument_errors_on_a_live_handle():
         assert np.array_equal(arr, oracle.stream(1000, 2, 0))
     finally:
         P.prng_destroy(h)
+
+
+def test_randomised_configurations():
+    """Seeded fuzz over the option space: numrn, numiter, seed, mode, batch size, kernel
+    variant, output transform, time-parallel on/off and how the run is split into calls;
+    every output vs the oracle."""
+    r = np.random.default_rng(20261017)
+    nvar = P.prng_kernel_variants()
+    names = [P.prng_kernel_variant_name(k) for k in range(nvar)]
+    usable = [k for k in range(nvar) if names[k] != "v2n4s1t"]
+    for trial in range(40):
+        n = int(r.choice([1, 2, 3, 31, 64, 100, 1000, 4096, 5003, 20000]))
+        i = int(r.choice([1, 2, 5, 17, 130, 600]))
+        seed = int(r.integers(0, 1 << 63))
+        mode = int(r.integers(0, 5))
+        if mode == P.PRNG_MODE_ZEROCOPY and n % 4:
+            mode = P.PRNG_MODE_OVERLAP2
+        kv = int(r.choice(usable))
+        star = int(kv < 4 and r.random() < 0.3)
+        tp = int(r.random() < 0.8)
+        batch = int(r.choice([0, 1, 3, 50]))
+        cuts = sorted({int(c) for c in r.integers(1, i, size=2)}) if i > 2 else []
+        calls = [b - a for a, b in zip([0] + cuts, cuts + [i])]
+        h = P.prng_create(n, seed)
+        try:
+            for opt, val in [(P.PRNG_OPT_MODE, mode), (P.PRNG_OPT_KERNEL, kv), (P.PRNG_OPT_OUTPUT, star),
+                             (P.PRNG_OPT_TIME_PARALLEL, tp), (P.PRNG_OPT_BATCH_ITERS, batch)]:
+                P.prng_set_option(h, opt, val)
+            out = np.zeros((i, n), np.uint64)
+            sink = P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0)
+            P.prng_init(h)
+            for c in calls:
+                P.prng_generate(h, c, P.SINK_COPY, sink)
+        finally:
+            P.prng_destroy(h)
+        want = oracle.stream_star(n, i, seed) if star else oracle.stream(n, i, seed)
+        assert np.array_equal(out, want), dict(trial=trial, n=n, i=i, mode=mode, kernel=names[kv], star=star,
+                                               tp=tp, batch=batch, calls=calls)
