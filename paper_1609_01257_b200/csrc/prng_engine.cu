@@ -57,6 +57,8 @@ const Variant kVariants[] = {
     // long per-CTA chunks: 32 / 64 numbers per thread (16 / 32 KiB per warp per iteration)
     // (measured: no gain over v2n4s1; 64 numbers/thread spills and was removed)
     V("v2n32s1", 2, 32, 0, 1, 1, 4),  V("v4n32s1", 4, 32, 0, 1, 1, 4),
+    // fewer instructions per number (32-B stores, more numbers per thread): less SM power
+    V("v4n12s1", 4, 12, 0, 1, 1, 4),  V("v4n16s1", 4, 16, 0, 1, 1, 4),
     // store cache policies on the default structure: .cs, L2::evict_first, L1::no_allocate
     V("v2n4s1cs", 2, 4, 1, 1, 1, 4),  V("v2n4s1ef", 2, 4, 2, 1, 1, 4), V("v2n4s1na", 2, 4, 3, 1, 1, 4),
     // diagnostic: v2n4s1 + per-CTA %globaltimer trace (PRNG_OPT_TRACE_PTR)
