@@ -132,3 +132,33 @@ def test_prof_calc_rejects_bad_input():
         P.prng_prof_calc([5], [0.0], [1.0], 4)
     with pytest.raises(P.PrngError):
         P.prng_prof_calc([0], [2.0], [1.0], 4)
+
+
+# ---------------------------------------------------------------- a6: properties (hypothesis)
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+_ev = st.lists(st.tuples(st.integers(0, 3), st.integers(0, 10_000), st.integers(0, 3_000)), max_size=25)
+
+
+@settings(max_examples=200, deadline=None)
+@given(_ev, st.integers(-50_000, 50_000))
+def test_prof_calc_properties(evs, shift):
+    """Union <= sum of durations; union >= longest event; union = sum - overlaps when no
+    instant is covered three times (S:427); everything invariant under a time shift;
+    per-name aggregates add up to the total."""
+    ids = [i for i, _, _ in evs]
+    s = [float(a) for _, a, _ in evs]
+    e = [float(a + d) for _, a, d in evs]
+    r = P.prng_prof_calc(ids, s, e, 4)
+    total = sum(b - a for a, b in zip(s, e))
+    assert r["agg"].sum() == pytest.approx(total)
+    assert r["effective"] <= total + 1e-9
+    if evs:
+        assert r["effective"] >= max(b - a for a, b in zip(s, e)) - 1e-9
+    rs = P.prng_prof_calc(ids, [x + shift for x in s], [x + shift for x in e], 4)
+    assert rs["effective"] == pytest.approx(r["effective"]) and np.allclose(rs["overlap"], r["overlap"])
+    cover = np.zeros(14_000, int)
+    for a, b in zip(s, e):
+        cover[int(a):int(b)] += 1
+    if cover.max(initial=0) <= 2:
+        assert r["effective"] == pytest.approx(total - np.triu(r["overlap"]).sum())
