@@ -271,6 +271,9 @@ double prng_probe_d2d_sweep_gbs(uint64_t chunk, uint64_t total, int reps); /* co
 /* research probe of SM store patterns (modes in prng_kernels.cuh store_pattern_kernel) */
 double prng_probe_store_mode_gbs(uint64_t bytes, int reps, int mode, int warps_per_cta, int ctas_per_sm,
                                  uint64_t slots);
+/* research probe: SM store kernel and copy-engine D2D sweep concurrently (combined GB/s) */
+double prng_probe_concurrent_gbs(uint64_t sm_bytes, uint64_t ce_bytes, uint64_t ce_chunk, int sm_warps, int reps,
+                                 double *sm_alone, double *ce_alone);
 
 #ifdef __cplusplus
 }

@@ -107,6 +107,7 @@ def lib():
         "prng_probe_d2h_gbs": ([u64, i32, i32, i32], dbl),
         "prng_probe_d2d_sweep_gbs": ([u64, u64, i32], dbl),
         "prng_probe_store_mode_gbs": ([u64, i32, i32, i32, i32, u64], dbl),
+        "prng_probe_concurrent_gbs": ([u64, u64, u64, i32, i32, PD, PD], dbl),
         "prng_sink_null": ([vp, u64, u32, u64, u64, P64], i32),
         "prng_sink_copy": ([vp, u64, u32, u64, u64, P64], i32),
         "prng_sink_digest": ([vp, u64, u32, u64, u64, P64], i32),

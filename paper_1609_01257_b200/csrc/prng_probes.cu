@@ -218,6 +218,83 @@ double prng_probe_store_mode_gbs(uint64_t bytes, int reps, int mode, int warps_p
     return cudaGetLastError() == cudaSuccess ? best : -1;
 }
 
+// Research probe: do the SM store path and the copy engine add up?  An SM store kernel
+// (grid-stride, `sm_warps` warps per SM) over `sm_bytes` on one stream while the copy
+// engine sweeps `ce_bytes` from an L2-resident `ce_chunk` source on another; returns the
+// combined destination GB/s (best of reps) and, via the out pointers, each side alone.
+double prng_probe_concurrent_gbs(uint64_t sm_bytes, uint64_t ce_bytes, uint64_t ce_chunk, int sm_warps, int reps,
+                                 double *sm_alone, double *ce_alone) {
+    uint64_t *a = nullptr, *src = nullptr, *b = nullptr;
+    if (cudaMalloc(&a, sm_bytes) != cudaSuccess) return -1;
+    if (cudaMalloc(&b, ce_bytes) != cudaSuccess || cudaMalloc(&src, ce_chunk) != cudaSuccess) {
+        cudaFree(a);
+        if (b) cudaFree(b);
+        return -1;
+    }
+    cudaMemset(src, 5, ce_chunk);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t s1, s2;
+    cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+    cudaEvent_t e0, e1, e2;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
+    auto sm_launch = [&](cudaStream_t s) {
+        probek::store_probe_kernel<<<sms, 32 * sm_warps, 0, s>>>(a, sm_bytes / 32, 0);
+    };
+    auto ce_launch = [&](cudaStream_t s) {
+        for (uint64_t off = 0; off + ce_chunk <= ce_bytes; off += ce_chunk)
+            cudaMemcpyAsync((char *)b + off, src, ce_chunk, cudaMemcpyDeviceToDevice, s);
+    };
+    const uint64_t ce_done = (ce_bytes / ce_chunk) * ce_chunk;
+    double best = 0, best_sm = 0, best_ce = 0;
+    for (int r = 0; r < reps + 1; ++r) {
+        float ms = 0;
+        // SM alone
+        cudaEventRecord(e0, s1);
+        sm_launch(s1);
+        cudaEventRecord(e1, s1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r) best_sm = std::max(best_sm, sm_bytes / (ms * 1e-3) / 1e9);
+        // CE alone
+        cudaEventRecord(e0, s2);
+        ce_launch(s2);
+        cudaEventRecord(e1, s2);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r) best_ce = std::max(best_ce, ce_done / (ms * 1e-3) / 1e9);
+        // both at once: both streams start after e0, the region ends when both are done
+        cudaDeviceSynchronize();
+        cudaEventRecord(e0, s1);
+        cudaStreamWaitEvent(s2, e0, 0);
+        sm_launch(s1);
+        ce_launch(s2);
+        cudaEventRecord(e1, s1);
+        cudaEventRecord(e2, s2);
+        cudaEventSynchronize(e1);
+        cudaEventSynchronize(e2);
+        float m1 = 0, m2 = 0;
+        cudaEventElapsedTime(&m1, e0, e1);
+        cudaEventElapsedTime(&m2, e0, e2);
+        if (r) best = std::max(best, (sm_bytes + ce_done) / (std::max(m1, m2) * 1e-3) / 1e9);
+    }
+    if (sm_alone) *sm_alone = best_sm;
+    if (ce_alone) *ce_alone = best_ce;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaStreamDestroy(s1);
+    cudaStreamDestroy(s2);
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(src);
+    return cudaGetLastError() == cudaSuccess ? best : -1;
+}
+
 double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams) {
     if (nstreams < 1) nstreams = 1;
     void *d = nullptr, *hbuf = nullptr;
