@@ -735,3 +735,37 @@ def test_randomised_configurations():
         want = oracle.stream_star(n, i, seed) if star else oracle.stream(n, i, seed)
         assert np.array_equal(out, want), dict(trial=trial, n=n, i=i, mode=mode, kernel=names[kv], star=star,
                                                tp=tp, batch=batch, calls=calls)
+
+
+@pytest.mark.slow
+def test_bench_config_every_iteration_no_ring():
+    """The bench kernel at the bench shape (2^24 x 1000, one launch, default variant and
+    grid) into a 134 GB device buffer with one slot per iteration (no wrap): all 1000
+    iterations folded per iteration (XOR, wrapping sum) on the GPU vs the oracle."""
+    import torch
+    n, i = 1 << 24, 1000
+    free, _ = torch.cuda.mem_get_info()
+    if free < 8 * n * i + (4 << 30):
+        pytest.skip("needs ~140 GB of free device memory")
+    buf = torch.empty((i, n), dtype=torch.int64, device="cuda")
+    h = P.prng_create(n, 0)
+    try:
+        P.prng_init(h)
+        P.prng_generate_device(h, i, buf.data_ptr(), n, i, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        sums = buf.sum(dim=1)  # int64 sums wrap mod 2^64
+        v = buf
+        m = n
+        while m > 1:  # XOR fold along gids, in place, one level per pass
+            h2 = m // 2
+            v[:, :h2] ^= v[:, m - h2:m]
+            m -= h2
+        xors = v[:, 0].clone()
+    finally:
+        P.prng_destroy(h)
+    got_s = sums.cpu().numpy().view(np.uint64)
+    got_x = xors.cpu().numpy().view(np.uint64)
+    del buf, v
+    torch.cuda.empty_cache()
+    wx, ws = _oracle_digest_threads(n, i, 0)
+    assert np.array_equal(got_x, wx) and np.array_equal(got_s, ws)
