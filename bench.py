@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--numrn-total", type=int, default=0, help="strong scaling: fixed total numrn (e.g. 2^28)")
     ap.add_argument("--numiter", type=int, default=DEF_NUMITER)
     ap.add_argument("--seed", type=int, default=SEED_PERF)
-    ap.add_argument("--kernel", type=int, default=0, help="kernel variant id (default 0 = v2n4s1; -1: prng_autotune)")
+    ap.add_argument("--kernel", type=int, default=0, help="kernel variant id (default 0 = v4n4s1; -1: prng_autotune)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--e2e-mode", type=int, default=3, help="0 S0, 1 S1, 2 O1, 3 O2, 4 O3 (zero-copy)")

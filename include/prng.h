@@ -162,7 +162,9 @@ enum prng_option {
                                   [CTA][round][iteration / 64] from variant "v2n4s1t"      */
     PRNG_OPT_OUTPUT = 10,      /* NEXT-3 output transform: 0 = the state (the paper, A7);
                                   1 = state * 0x2545F4914F6CDD1D mod 2^64 (xorshift64*-style
-                                  scrambler, A19).  Needs kernel variant 0..3.              */
+                                  scrambler, A19).  Needs a CTA-synchronised variant with
+                                  a scrambled instantiation (v4n4s1, v2n8s1, v2n16s1,
+                                  v4n8s1, v2n4s1); others give PRNG_EINVAL.            */
     PRNG_OPT_TIME_PARALLEL = 11, /* 1 (default): when numrn is too small to fill the GPU, cut
                                   a launch's iterations into chunks started by GF(2)
                                   jump-ahead (xs^k is linear: a 64x64 bit matrix); 0: off */
@@ -196,9 +198,10 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
  * PRNG_ESTATE otherwise).  best_gbs (may be NULL) gets the winner's probe GB/s. */
 int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err);
 
-/* Number of kernel variants compiled in, and the name of one ("v2n4s1" = 16-byte stores,
- * 4 numbers per thread, CTA barrier every iteration; "v4n8" = 32-byte stores, 8 numbers
- * per thread, free-running warps). */
+/* Number of kernel variants compiled in, and the name of one (id 0 "v4n4s1", the default:
+ * one 32-byte store per thread per iteration, 4 numbers per thread, CTA barrier every
+ * iteration; "v2n4s1" = the same with two 16-byte stores; "v4n8" = 32-byte stores, 8
+ * numbers per thread, free-running warps).  NULL for an id out of range. */
 int prng_kernel_variants(void);
 const char *prng_kernel_variant_name(int id);
 

@@ -37,17 +37,23 @@ struct Variant {
     int warps_per_sm;                     // default grid: resident warps per SM (0 = occupancy max)
     BatchFn fn;
     int stages;                           // > 0: TMA bulk-store kernel with this many smem stages
+    BatchFn star;                         // NEXT-3 xorshift64* output instantiation (nullptr: none)
 };
 #define V(name, vec, npt, pol, sync, cl, wps) \
-    {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>, 0}
-#define VT(name, npt, stages, wps) {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages}
+    {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>, 0, nullptr}
+// CTA-synchronised variants that also carry the NEXT-3 scrambled-output instantiation
+#define VS(name, vec, npt, wps) \
+    {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1>, 0, prngk::batch_kernel<vec, npt, 0, 1, 1>}
+#define VT(name, npt, stages, wps) {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages, nullptr}
 // Measured on B200 at numrn = 2^24 x 1000 through a non-reused 64 GiB ring
-// (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 16-B vectors reach
-// ~6.9 TB/s (93 % of the same-box cudaMemset fill rate); free-running warps at full
+// (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 16-/32-B vectors reach
+// 6.6-6.8 TB/s (~90 % of the same-box cudaMemset fill rate; one 32-B store per thread is
+// ~2 % ahead of two 16-B ones, 7.29 TB/s at numrn = 2^27); free-running warps at full
 // occupancy ~6.2 TB/s (more concurrently open DRAM pages).
 const Variant kVariants[] = {
-    V("v2n4s1", 2, 4, 0, 1, 1, 4),  // default: 16-B stores, 4 numbers/thread, CTA barrier, 4 warps/SM
-    V("v2n8s1", 2, 8, 0, 1, 1, 4),    V("v2n16s1", 2, 16, 0, 1, 1, 4), V("v4n8s1", 4, 8, 0, 1, 1, 4),
+    VS("v4n4s1", 4, 4, 4),  // default: one 32-B store per thread per iteration, 4 numbers/thread,
+                            // CTA barrier, 4 warps/SM (round-1 default v2n4s1 is id 28)
+    VS("v2n8s1", 2, 8, 4),  VS("v2n16s1", 2, 16, 4), VS("v4n8s1", 4, 8, 4),
     // free-running warps
     V("v4n8", 4, 8, 0, 0, 1, 0),      V("v2n4", 2, 4, 0, 0, 1, 0),     V("v2n8", 2, 8, 0, 0, 1, 0),
     V("v4n4", 4, 4, 0, 0, 1, 0),      V("v4n16", 4, 16, 0, 0, 1, 0),   V("v2n16", 2, 16, 0, 0, 1, 0),
@@ -66,15 +72,13 @@ const Variant kVariants[] = {
     // TMA bulk stores: one cp.async.bulk per warp per iteration from an smem stage ring
     VT("t2n4", 4, 4, 4),   VT("t2n8", 8, 4, 4),   VT("t2n16", 16, 4, 4),  VT("t2n8s8", 8, 8, 4),
     VT("t2n4w8", 4, 4, 8), VT("t2n8w8", 8, 4, 8),
+    // the round-1 default: two 16-B stores per thread per iteration (r1_sweeps.md "32-B stores")
+    VS("v2n4s1", 2, 4, 4),
 };
 #undef VT
+#undef VS
 #undef V
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
-// NEXT-3: the CTA-synchronised variants (ids 0..3) instantiated with the xorshift64*
-// output scrambler (PRNG_OPT_OUTPUT = 1), same grid policy.
-const BatchFn kStarFns[] = {prngk::batch_kernel<2, 4, 0, 1, 1>, prngk::batch_kernel<2, 8, 0, 1, 1>,
-                            prngk::batch_kernel<2, 16, 0, 1, 1>, prngk::batch_kernel<4, 8, 0, 1, 1>};
-constexpr int kNumStar = sizeof(kStarFns) / sizeof(kStarFns[0]);
 
 size_t variant_smem(const Variant &v, uint64_t warps_per_block) {
     return v.stages ? (size_t)warps_per_block * v.stages * 32 * v.npt * sizeof(uint64_t) : 0;
@@ -157,8 +161,8 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     const Variant &v0 = kVariants[h->kernel];
     Variant v = v0;
     if (h->output == 1) {
-        if (h->kernel >= kNumStar) return set_err(err, PRNG_EINVAL, "output scrambling needs kernel variant < %d", kNumStar);
-        v.fn = kStarFns[h->kernel];
+        if (!v0.star) return set_err(err, PRNG_EINVAL, "output scrambling not compiled for variant %s", v0.name);
+        v.fn = v0.star;
     }
     prngk::BatchArgs a;
     a.dst = dst;
@@ -446,8 +450,8 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             break;
         case PRNG_OPT_KERNEL:
             if (value < 0 || value >= kNumVariants) return set_err(err, PRNG_EINVAL, "bad kernel variant");
-            if (h->output == 1 && value >= kNumStar)
-                return set_err(err, PRNG_EINVAL, "output scrambling needs kernel variant < %d", kNumStar);
+            if (h->output == 1 && !kVariants[value].star)
+                return set_err(err, PRNG_EINVAL, "output scrambling not compiled for variant %s", kVariants[value].name);
             h->kernel = (int)value;
             break;
         case PRNG_OPT_TIME_PARALLEL:
@@ -459,8 +463,8 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             break;
         case PRNG_OPT_OUTPUT:
             if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad output transform");
-            if (value == 1 && h->kernel >= kNumStar)
-                return set_err(err, PRNG_EINVAL, "output scrambling needs kernel variant < %d", kNumStar);
+            if (value == 1 && !kVariants[h->kernel].star)
+                return set_err(err, PRNG_EINVAL, "output scrambling not compiled for variant %s", kVariants[h->kernel].name);
             h->output = (int)value;
             break;
         case PRNG_OPT_GRID_WARPS:
@@ -662,7 +666,7 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
 static const struct {
     const char *variant;
     int warps_per_sm;
-} kTuneCandidates[] = {{"v2n4s1", 4}, {"v2n4s1", 8}, {"v2n8s1", 4}, {"v2n8s1", 8},
+} kTuneCandidates[] = {{"v4n4s1", 4}, {"v2n4s1", 4}, {"v2n4s1", 8}, {"v2n8s1", 4},
                        {"v2n16s1", 4}, {"v2n8c2", 4}, {"v4n8s1", 4}, {"t2n8w8", 8}};
 
 extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err) {

@@ -9,6 +9,13 @@ import oracle
 import paper_1609_01257_b200 as P
 from workloads import RAGGED_N, SEED_PARITY, SPEC_GRID_I, SPEC_GRID_N, sample_points, shard_range
 
+# variants compiled with the NEXT-3 scrambled-output instantiation (prng_engine.cu VS(...))
+STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1")
+
+
+def _kid(name):
+    return [P.prng_kernel_variant_name(k) for k in range(P.prng_kernel_variants())].index(name)
+
 pytestmark = pytest.mark.gpu
 
 
@@ -176,7 +183,7 @@ def test_autotune_then_parity():
     assert np.array_equal(out, oracle.stream(n, i, SEED_PARITY))
 
 
-@pytest.mark.parametrize("kv", range(30))
+@pytest.mark.parametrize("kv", range(32))
 def test_every_variant_device_only_wrapping_ring(kv):
     """Each kernel variant through the device-only ring path (grid-strided rounds, ring
     wrap-around inside one launch), vs the oracle at the ring slots and the state."""
@@ -328,9 +335,10 @@ def test_host_memory_kinds(kind):
     assert np.array_equal(out, oracle.stream(n, i, 3))
 
 
-@pytest.mark.parametrize("kv", range(4))
-def test_star_output_all_paths(kv):
+@pytest.mark.parametrize("kname", STAR_NAMES)
+def test_star_output_all_paths(kname):
     """NEXT-3 (A19): scrambled output through e2e (O2, O3) and device-only, vs the oracle."""
+    kv = _kid(kname)
     n, i = 4100, 7
     want = oracle.stream_star(n, i, 6)
     for mode in (P.PRNG_MODE_OVERLAP2, P.PRNG_MODE_ZEROCOPY):
@@ -365,9 +373,13 @@ def test_star_output_all_paths(kv):
 def test_star_output_rejects_other_variants():
     h = P.prng_create(64, 0)
     try:
-        P.prng_set_option(h, P.PRNG_OPT_KERNEL, 5)
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid("v2n4"))
         with pytest.raises(P.PrngError):
             P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid("v2n4s1"))
+        P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
+        with pytest.raises(P.PrngError):  # and the other order
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid("t2n8"))
     finally:
         P.prng_destroy(h)
 
@@ -419,8 +431,9 @@ def test_time_parallel_off_is_identical():
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], oracle.stream(n, i, 5))
 
 
-@pytest.mark.parametrize("kv", range(4))
-def test_time_parallel_star(kv):
+@pytest.mark.parametrize("kname", STAR_NAMES)
+def test_time_parallel_star(kname):
+    kv = _kid(kname)
     n, i = 512, 1333
     h = P.prng_create(n, 2)
     try:
@@ -715,7 +728,7 @@ def test_randomised_configurations():
         if mode == P.PRNG_MODE_ZEROCOPY and n % 4:
             mode = P.PRNG_MODE_OVERLAP2
         kv = int(r.choice(usable))
-        star = int(kv < 4 and r.random() < 0.3)
+        star = int(names[kv] in STAR_NAMES and r.random() < 0.3)
         tp = int(r.random() < 0.8)
         batch = int(r.choice([0, 1, 3, 50]))
         cuts = sorted({int(c) for c in r.integers(1, i, size=2)}) if i > 2 else []
