@@ -171,8 +171,17 @@ enum prng_option {
     PRNG_OPT_BLOCKING = 12,    /* 1 (default): device-only prng_generate returns when the work
                                   is done; 0: returns after enqueueing on the generation
                                   stream (synchronise the stream before reading results)   */
-    PRNG_OPT_CTA_WARPS = 13    /* warps per CTA of the batch kernels (1..8); 0 = auto: one
+    PRNG_OPT_CTA_WARPS = 13,   /* warps per CTA of the batch kernels (1..8); 0 = auto: one
                                   CTA per SM when <= 8 warps per SM are used               */
+    PRNG_OPT_CHUNK_ITERS = 14, /* L > 0: cut every launch of more than L iterations into
+                                  chunks of L started by GF(2) jump-ahead, at any numrn
+                                  (the work order of time-parallel mode); 0 (default): only
+                                  as PRNG_OPT_TIME_PARALLEL decides.  Output unchanged.     */
+    PRNG_OPT_PIECE_ORDER = 15  /* how work units are dealt to warps (output unchanged):
+                                  0 (default) round-robin, adjacent CTAs hold adjacent
+                                  pieces; 1 CTA-blocked, CTA b holds a contiguous run of
+                                  units, so concurrently written 4 KiB chunks are spread
+                                  over the whole slot.  Not for cluster variants.          */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two

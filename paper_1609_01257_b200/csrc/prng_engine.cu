@@ -178,6 +178,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     a.chunk_len = iters;
     a.jump = nullptr;
     a.state_out = h->d_state;
+    a.order = (v.stages == 0 && v.cluster <= 1) ? (uint32_t)h->piece_order : 0u;
 
     const uint64_t piece = 32ull * v.npt;
     a.npieces = (h->count + piece - 1) / piece;
@@ -193,35 +194,37 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // pieces x chunks units fill it.
     uint64_t units = a.npieces;
     // (chunks >= 256 iterations keep the per-unit 64-step mat-vec below ~10 % of its work)
-    if (h->time_parallel && v.stages == 0 && 2 * a.npieces <= max_warps && iters >= 512) {
-        uint64_t C = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
-        if (C > 1) {
-            const uint64_t L = (iters + C - 1) / C;
-            C = (iters + L - 1) / L;
-            if (C > h->jump_cap) {
-                if (h->d_jump) cudaFree(h->d_jump);
-                h->d_jump = nullptr;
-                h->jump_cap = 0;
-                CU(cudaMalloc(&h->d_jump, C * 64 * sizeof(uint64_t)));
-                h->jump_cap = C;
-                h->jump_key[0] = 0;
-            }
-            const uint64_t e = first_is_state ? 0 : 1;
-            if (h->jump_key[0] != C || h->jump_key[1] != L || h->jump_key[2] != e) {
-                prngk::jump_columns_kernel<<<1, 64, 0, s>>>(h->d_jump, (uint32_t)C, (uint64_t)L, (uint32_t)e);
-                CU(cudaGetLastError());
-                h->jump_key[0] = C;
-                h->jump_key[1] = L;
-                h->jump_key[2] = e;
-            }
-            if (!h->d_state2)  // allocated on first use: small numrn only
-                CU(cudaMalloc(&h->d_state2, pitch_for(h->count) * sizeof(uint64_t)));
-            a.nchunks = (uint32_t)C;
-            a.chunk_len = (uint32_t)L;
-            a.jump = h->d_jump;
-            a.state_out = h->d_state2;  // chunks read d_state; the last chunk writes the other half
-            units = a.npieces * C;
+    uint64_t nch = 0;
+    if (v.stages == 0 && h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters)
+        nch = (iters + h->chunk_iters - 1) / h->chunk_iters;  // PRNG_OPT_CHUNK_ITERS: forced
+    else if (h->time_parallel && v.stages == 0 && 2 * a.npieces <= max_warps && iters >= 512)
+        nch = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
+    if (nch > 1) {
+        const uint64_t L = (iters + nch - 1) / nch;
+        const uint64_t C = (iters + L - 1) / L;
+        if (C > h->jump_cap) {
+            if (h->d_jump) cudaFree(h->d_jump);
+            h->d_jump = nullptr;
+            h->jump_cap = 0;
+            CU(cudaMalloc(&h->d_jump, C * 64 * sizeof(uint64_t)));
+            h->jump_cap = C;
+            h->jump_key[0] = 0;
         }
+        const uint64_t e = first_is_state ? 0 : 1;
+        if (h->jump_key[0] != C || h->jump_key[1] != L || h->jump_key[2] != e) {
+            prngk::jump_columns_kernel<<<1, 64, 0, s>>>(h->d_jump, (uint32_t)C, (uint64_t)L, (uint32_t)e);
+            CU(cudaGetLastError());
+            h->jump_key[0] = C;
+            h->jump_key[1] = L;
+            h->jump_key[2] = e;
+        }
+        if (!h->d_state2)  // allocated on first use: small numrn only
+            CU(cudaMalloc(&h->d_state2, pitch_for(h->count) * sizeof(uint64_t)));
+        a.nchunks = (uint32_t)C;
+        a.chunk_len = (uint32_t)L;
+        a.jump = h->d_jump;
+        a.state_out = h->d_state2;  // chunks read d_state; the last chunk writes the other half
+        units = a.npieces * C;
     }
     const uint64_t rounds0 = (units + max_warps - 1) / max_warps;
     uint64_t warps = (units + rounds0 - 1) / rounds0;
@@ -482,6 +485,14 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
         case PRNG_OPT_TRACE_PTR:
             h->trace = (unsigned long long *)(uintptr_t)value;
             break;
+        case PRNG_OPT_CHUNK_ITERS:
+            if (value < 0 || value > 0xFFFFFFFFll) return set_err(err, PRNG_EINVAL, "bad chunk iterations");
+            h->chunk_iters = value;
+            break;
+        case PRNG_OPT_PIECE_ORDER:
+            if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad piece order");
+            h->piece_order = (int)value;
+            break;
 
 
         default:
@@ -506,6 +517,8 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_RING_PAD: *value = h->ring_pad; break;
         case PRNG_OPT_HOST_MEM: *value = h->host_mem; break;
         case PRNG_OPT_TRACE_PTR: *value = (int64_t)(uintptr_t)h->trace; break;
+        case PRNG_OPT_CHUNK_ITERS: *value = h->chunk_iters; break;
+        case PRNG_OPT_PIECE_ORDER: *value = h->piece_order; break;
 
 
         default: return set_err(err, PRNG_EINVAL, "unknown option %d", option);

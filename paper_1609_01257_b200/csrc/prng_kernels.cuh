@@ -178,6 +178,8 @@ struct BatchArgs {
     uint32_t chunk_len;
     const uint64_t *jump;     // [nchunks][64] (nchunks > 1)
     uint64_t *state_out;      // nchunks > 1: the last chunk writes the final state here
+    uint32_t order;           // 0: unit r*W + w to warp w in round r (adjacent CTAs, adjacent
+                              //    pieces); 1: CTA b takes units [b*rounds*wpb, (b+1)*rounds*wpb)
 };
 
 // y = J x over GF(2): XOR of the columns J e_i selected by the bits of x (xs^k is linear).
@@ -418,7 +420,9 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     const uint64_t cta_warp0 = (uint64_t)blockIdx.x * wpb;
     const uint64_t nunits = a.npieces * (a.nchunks ? a.nchunks : 1);
     for (uint32_t r = 0; r < a.rounds; ++r) {
-        const uint64_t unit = (uint64_t)r * nwarps + warp;
+        // unit index of this CTA's warp 0 in round r; the CTA's warps hold consecutive units
+        const uint64_t first = a.order ? ((uint64_t)blockIdx.x * a.rounds + r) * wpb : (uint64_t)r * nwarps + cta_warp0;
+        const uint64_t unit = first + (warp - cta_warp0);
         if (unit >= nunits) {  // warp-uniform
             if constexpr (SYNC == 2) {
                 Unit u = make_unit<NPT, VEC>(a, 0, lane);
@@ -432,7 +436,6 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
         }
         const Unit u = make_unit<NPT, VEC>(a, unit, lane);
         // warps of this CTA holding a unit in round r: a prefix of the CTA's warps
-        const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
         const uint32_t bar_threads = 32u * (uint32_t)(nunits - first < wpb ? nunits - first : wpb);
         const uint64_t piece = unit % a.npieces;
         if ((piece + 1) * PIECE <= a.count)

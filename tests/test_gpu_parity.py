@@ -431,6 +431,64 @@ def test_time_parallel_off_is_identical():
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], oracle.stream(n, i, 5))
 
 
+@pytest.mark.parametrize("order", [0, 1])
+@pytest.mark.parametrize("chunk", [0, 1, 37, 300])
+@pytest.mark.parametrize("kname", ["v4n4s1", "v2n8", "v2n4s1"])
+def test_forced_chunks_and_piece_order(kname, chunk, order):
+    """PRNG_OPT_CHUNK_ITERS (jump-started chunks at any numrn) and PRNG_OPT_PIECE_ORDER
+    (CTA-blocked dealing) change only the work order: every output, split calls included,
+    and the final state vs the oracle; ragged numrn spanning several rounds of pieces."""
+    n, i = 70001, 777
+    want = oracle.stream(n, i, SEED_PARITY)
+    for calls in ([i], [400, 1, 376]):
+        h = P.prng_create(n, SEED_PARITY)
+        try:
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid(kname))
+            P.prng_set_option(h, P.PRNG_OPT_CHUNK_ITERS, chunk)
+            P.prng_set_option(h, P.PRNG_OPT_PIECE_ORDER, order)
+            P.prng_set_option(h, P.PRNG_OPT_GRID_WARPS, 96)  # several rounds per warp
+            out = np.zeros((i, n), np.uint64)
+            sink = P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0)
+            P.prng_init(h)
+            for c in calls:
+                P.prng_generate(h, c, P.SINK_COPY, sink)
+            st = P.prng_read_state(h, n)
+        finally:
+            P.prng_destroy(h)
+        assert np.array_equal(out, want), (calls, chunk, order)
+        assert np.array_equal(st, want[-1])
+
+
+def test_forced_chunks_device_only_bench_shape():
+    """Forced chunks + CTA-blocked order at the bench width (2^24), device-only into a
+    torch buffer: every iteration's XOR and wrapping sum of all 2^24 outputs (folded on the
+    GPU) vs the oracle's per-iteration digests, and the final state."""
+    import torch
+    n, i = 1 << 24, 48
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_CHUNK_ITERS, 10)
+        P.prng_set_option(h, P.PRNG_OPT_PIECE_ORDER, 1)
+        buf = torch.empty((i, n), dtype=torch.int64, device="cuda")
+        P.prng_init(h)
+        P.prng_generate_device(h, i, buf.data_ptr(), n, i, 0)
+        torch.cuda.synchronize()
+        got_s = [int(v) & ((1 << 64) - 1) for v in buf.sum(dim=1).tolist()]  # int64 sum wraps mod 2^64
+        v, m = buf.clone(), n
+        while m > 1:
+            h2 = m // 2
+            v[:, :h2] ^= v[:, m - h2:m]
+            m -= h2
+        got_x = [int(x) & ((1 << 64) - 1) for x in v[:, 0].tolist()]
+        last = buf[-1].cpu().numpy().view(np.uint64)
+        st = P.prng_read_state(h, n)
+    finally:
+        P.prng_destroy(h)
+    wx, ws = _oracle_digest_threads(n, i, SEED_PARITY)
+    assert got_x == [int(x) for x in wx] and got_s == [int(x) for x in ws]
+    assert np.array_equal(st, last)
+
+
 @pytest.mark.parametrize("kname", STAR_NAMES)
 def test_time_parallel_star(kname):
     kv = _kid(kname)
