@@ -177,11 +177,20 @@ enum prng_option {
                                   chunks of L started by GF(2) jump-ahead, at any numrn
                                   (the work order of time-parallel mode); 0 (default): only
                                   as PRNG_OPT_TIME_PARALLEL decides.  Output unchanged.     */
-    PRNG_OPT_PIECE_ORDER = 15  /* how work units are dealt to warps (output unchanged):
+    PRNG_OPT_PIECE_ORDER = 15, /* how work units are dealt to warps (output unchanged):
                                   0 (default) round-robin, adjacent CTAs hold adjacent
                                   pieces; 1 CTA-blocked, CTA b holds a contiguous run of
                                   units, so concurrently written 4 KiB chunks are spread
                                   over the whole slot.  Not for cluster variants.          */
+    PRNG_OPT_EPOCH_ITERS = 16  /* epoch-major order for CTA-synchronised variants (output
+                                  unchanged): every warp runs each of its pieces through E
+                                  iterations, then the next piece; the state goes through
+                                  HBM between epochs (+16 B per number per epoch).
+                                  0 (default) auto: E = R when a device-only launch wraps
+                                  a ring of R slots whose live lines (R x grid warps x
+                                  bytes per warp-iteration) are < 2x L2, so no address is
+                                  rewritten while its line may still be in L2 (DESIGN.md
+                                  §5); E > 0 forced; -1 off.                                */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two

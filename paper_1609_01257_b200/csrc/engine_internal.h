@@ -97,6 +97,7 @@ struct prng {
     int64_t batch_iters = 0, ring_slots_opt = 0, grid_warps = 0, ring_pad = 0, cta_warps = 0;
     int64_t chunk_iters = 0;  // PRNG_OPT_CHUNK_ITERS
     int piece_order = 0;      // PRNG_OPT_PIECE_ORDER
+    int64_t epoch_iters = 0;  // PRNG_OPT_EPOCH_ITERS
     unsigned long long *trace = nullptr;  // PRNG_OPT_TRACE_PTR (diagnostic variant only)
 
     int profile = 0, kernel = 0, output = 0, blocking = 1;

@@ -38,13 +38,17 @@ struct Variant {
     BatchFn fn;
     int stages;                           // > 0: TMA bulk-store kernel with this many smem stages
     BatchFn star;                         // NEXT-3 xorshift64* output instantiation (nullptr: none)
+    BatchFn epoch, epoch_star;            // epoch-major instantiations (nullptr: none)
 };
 #define V(name, vec, npt, pol, sync, cl, wps) \
-    {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>, 0, nullptr}
-// CTA-synchronised variants that also carry the NEXT-3 scrambled-output instantiation
-#define VS(name, vec, npt, wps) \
-    {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1>, 0, prngk::batch_kernel<vec, npt, 0, 1, 1>}
-#define VT(name, npt, stages, wps) {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages, nullptr}
+    {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>, 0, nullptr, nullptr, nullptr}
+// CTA-synchronised variants that also carry the NEXT-3 scrambled-output and the
+// epoch-major instantiations
+#define VS(name, vec, npt, wps)                                                                            \
+    {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1>, 0, prngk::batch_kernel<vec, npt, 0, 1, 1>, \
+     prngk::batch_kernel_epoch<vec, npt, 0>, prngk::batch_kernel_epoch<vec, npt, 1>}
+#define VT(name, npt, stages, wps) \
+    {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages, nullptr, nullptr, nullptr}
 // Measured on B200 at numrn = 2^24 x 1000 through a non-reused 64 GiB ring
 // (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 16-/32-B vectors reach
 // 6.6-6.8 TB/s (~90 % of the same-box cudaMemset fill rate; one 32-B store per thread is
@@ -199,7 +203,25 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
         nch = (iters + h->chunk_iters - 1) / h->chunk_iters;  // PRNG_OPT_CHUNK_ITERS: forced
     else if (h->time_parallel && v.stages == 0 && 2 * a.npieces <= max_warps && iters >= 512)
         nch = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
-    if (nch > 1) {
+    // Epoch-major order (batch_kernel_epoch, DESIGN.md §5 "L2 absorption"): when a launch
+    // wraps the ring and the natural order would rewrite an address while its line can
+    // still be in L2 (the grid rewrites its pieces' R slots every R iterations: R x warps x
+    // bytes per warp-iteration of live lines), cut the launch into epochs of E = R
+    // iterations, so an address is rewritten only one whole epoch (the full ring) later.
+    uint64_t E = 0;
+    if (v.epoch && nch <= 1 && h->epoch_iters >= 0) {
+        const uint64_t live = nslots * std::min<uint64_t>(max_warps, a.npieces) * piece * sizeof(uint64_t);
+        if (h->epoch_iters > 0)
+            E = (uint64_t)h->epoch_iters;  // PRNG_OPT_EPOCH_ITERS: forced
+        else if (iters > nslots && live < 2 * (uint64_t)h->l2_bytes)
+            E = nslots;
+        if (E >= iters) E = 0;
+    }
+    if (E > 0) {
+        v.fn = h->output == 1 ? v0.epoch_star : v0.epoch;
+        a.nchunks = (uint32_t)((iters + E - 1) / E);
+        a.chunk_len = (uint32_t)E;
+    } else if (nch > 1) {
         const uint64_t L = (iters + nch - 1) / nch;
         const uint64_t C = (iters + L - 1) / L;
         if (C > h->jump_cap) {
@@ -268,7 +290,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     } else {
         v.fn<<<(unsigned)blocks, (unsigned)(32 * wpb), variant_smem(v, wpb), s>>>(a);
     }
-    if (a.nchunks > 1) std::swap(h->d_state, h->d_state2);  // the final state is in the other half
+    if (a.jump) std::swap(h->d_state, h->d_state2);  // time-parallel: the final state is in the other half
     CU(cudaGetLastError());
     return prof_end(h, s, err);
 }
@@ -493,6 +515,10 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad piece order");
             h->piece_order = (int)value;
             break;
+        case PRNG_OPT_EPOCH_ITERS:
+            if (value < -1 || value > 0xFFFFFFFFll) return set_err(err, PRNG_EINVAL, "bad epoch iterations");
+            h->epoch_iters = value;
+            break;
 
 
         default:
@@ -519,6 +545,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_TRACE_PTR: *value = (int64_t)(uintptr_t)h->trace; break;
         case PRNG_OPT_CHUNK_ITERS: *value = h->chunk_iters; break;
         case PRNG_OPT_PIECE_ORDER: *value = h->piece_order; break;
+        case PRNG_OPT_EPOCH_ITERS: *value = h->epoch_iters; break;
 
 
         default: return set_err(err, PRNG_EINVAL, "unknown option %d", option);

@@ -445,6 +445,158 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- a2+a3, epoch-major order
+// Measured (profiles/r1_sweeps.md, "Concurrently written slots"): the write stream slows
+// down when the grid writes into many ring slots (= iterations) at once.  batch_kernel
+// runs each piece through all T iterations of the launch; the CTAs drift apart by ~180
+// iterations, so ~148 slots are written concurrently.  Here the launch is cut into epochs
+// of E iterations: in epoch e every warp runs each of its pieces (piece r*W + w, r =
+// 0, 1, ...) through iterations [eE, eE + E), keeping the state in registers inside an
+// epoch and in d_state between epochs.  Only the <= E slots of the current epoch (two at
+// an epoch boundary) are being written.  Extra traffic: 16 B per number per epoch
+// (2/E of the output).
+//
+// Every piece of a warp is always run by the same lanes, so a state written at the end
+// of one unit is read back by the thread that wrote it (program order; no grid sync).
+// The next unit's state is prefetched while the current unit runs (a load issued behind
+// a saturated write stream takes ~1 us), which needs >= 2 pieces per warp (the host
+// checks npieces >= 2 W); the load is .cg, as the state is rewritten during the launch.
+// CTA barrier every iteration as in SYNC 1.
+__device__ __forceinline__ void ld_v4_cg(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
+    asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+__device__ __forceinline__ void ld_v2_cg(const uint64_t *p, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+template <int VEC>
+__device__ __forceinline__ void load_vec_cg(const uint64_t *p, uint64_t *x) {
+    if constexpr (VEC == 4)
+        ld_v4_cg(p, x[0], x[1], x[2], x[3]);
+    else
+        ld_v2_cg(p, x[0], x[1]);
+}
+
+// One unit of the epoch kernel: a piece through iterations [t_begin, t_begin + t_count).
+template <int VEC, int NPT, int OUT, bool FULL>
+__device__ __forceinline__ void epoch_unit(const BatchArgs &a, uint64_t *x, uint64_t base, uint32_t slot,
+                                           uint32_t t_count, bool emit_first, uint32_t bar_threads) {
+    constexpr int NV = NPT / VEC;
+    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
+    uint64_t *p = a.dst + (uint64_t)slot * a.pitch + base;
+    auto trip = [&]() {
+        if constexpr (FULL) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                uint64_t y[VEC];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) y[q] = emit<OUT>(x[v * VEC + q]);
+                store_vec<VEC, 0>(p + v * 32 * VEC, y);
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+                for (int q = 0; q < VEC; ++q)
+                    if (base + (uint64_t)v * 32 * VEC + q < a.count) p[v * 32 * VEC + q] = emit<OUT>(x[v * VEC + q]);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+        if (++slot == a.nslots) {  // warp-uniform
+            slot = 0;
+            p -= wrap;
+        } else {
+            p += a.pitch;
+        }
+    };
+    auto step = [&]() {
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
+    };
+    if (!emit_first) step();
+    trip();
+    for (uint32_t t = 1; t < t_count; ++t) {  // the hot loop
+        step();
+        trip();
+    }
+}
+
+template <int VEC, int NPT, int OUT = 0>
+__global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
+    static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
+    constexpr int NV = NPT / VEC;
+    constexpr uint64_t PIECE = 32ull * NPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t cta_warp0 = (uint64_t)blockIdx.x * wpb;
+    const uint64_t warp = cta_warp0 + (threadIdx.x >> 5);
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    if (warp >= a.npieces) return;  // warp-uniform; such warps are never counted in bar_threads
+    const uint64_t kw = (a.npieces - warp + nwarps - 1) / nwarps;  // pieces of this warp
+    // Every warp of the CTA that has pieces takes part in every barrier of every round up to
+    // the CTA's last (its warp 0 has the most pieces): a warp without a piece in a round
+    // idles through that round's barriers, so the CTA's warps never run into different
+    // rounds (or epochs) on the same named barrier.
+    const uint64_t kw_cta = (a.npieces - cta_warp0 + nwarps - 1) / nwarps;
+    const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - cta_warp0 < wpb ? a.npieces - cta_warp0 : wpb);
+    const bool prefetch = kw >= 2;  // kw == 1: the next unit is this piece again (not written yet)
+    const uint32_t E = a.chunk_len;
+    auto is_full = [&](uint64_t piece) { return (piece + 1) * PIECE <= a.count; };
+    auto lane_base = [&](uint64_t piece) { return piece * PIECE + (uint64_t)lane * VEC; };
+    auto load_full = [&](uint64_t piece, uint64_t *dst) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) load_vec_cg<VEC>(a.state + lane_base(piece) + (uint64_t)v * 32 * VEC, dst + v * VEC);
+    };
+    uint64_t xn[NPT];  // prefetched state of the next unit (full pieces)
+    if (prefetch && is_full(warp)) load_full(warp, xn);
+    for (uint32_t e = 0; e < a.nchunks; ++e) {
+        const uint32_t t_begin = e * E;
+        const uint32_t t_count = a.iters - t_begin < E ? a.iters - t_begin : E;
+        const bool emit_first = e == 0 && a.first_is_state;
+        const uint32_t slot_begin = (uint32_t)(((uint64_t)a.slot0 + t_begin) % a.nslots);
+        for (uint64_t r = 0; r < kw_cta; ++r) {
+            if (r >= kw) {  // no piece for this warp in round r: idle through its barriers
+                for (uint32_t t = 0; t < t_count; ++t) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+                continue;
+            }
+            const uint64_t piece = r * nwarps + warp;
+            const uint64_t base = lane_base(piece);
+            uint64_t x[NPT];
+            if (is_full(piece)) {
+                if (prefetch) {
+#pragma unroll
+                    for (int j = 0; j < NPT; ++j) x[j] = xn[j];
+                    // the next unit: the next piece of this epoch, or the warp's first piece of
+                    // the next epoch (its state was written at the end of this epoch's unit 0)
+                    const uint64_t np = r + 1 < kw ? piece + nwarps : warp;
+                    if ((r + 1 < kw || e + 1 < a.nchunks) && is_full(np)) load_full(np, xn);
+                } else {
+                    load_full(piece, x);
+                }
+                epoch_unit<VEC, NPT, OUT, true>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+            } else {  // the ragged last piece (its successor, if any, is never a full piece of
+                      // a later round: it is the last piece)
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) {
+                        const uint64_t idx = base + (uint64_t)v * 32 * VEC + q;
+                        x[v * VEC + q] = idx < a.count ? __ldcg(a.state + idx) : 0ull;
+                    }
+                if (prefetch && e + 1 < a.nchunks && is_full(warp)) load_full(warp, xn);
+                epoch_unit<VEC, NPT, OUT, false>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) {
+                        const uint64_t idx = base + (uint64_t)v * 32 * VEC + q;
+                        if (idx < a.count) a.state[idx] = x[v * VEC + q];
+                    }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- a2+a3 with TMA bulk stores
 // Same work decomposition (VEC = 2), but each iteration's piece is staged in shared
 // memory (STS.128, same lane layout) and written to HBM by ONE bulk async copy per warp

@@ -459,6 +459,59 @@ def test_forced_chunks_and_piece_order(kname, chunk, order):
         assert np.array_equal(st, want[-1])
 
 
+@pytest.mark.parametrize("out_kind", [0, 1])
+@pytest.mark.parametrize("epoch", [1, 3, 64])
+@pytest.mark.parametrize("kname", STAR_NAMES)
+def test_epoch_order(kname, epoch, out_kind):
+    """PRNG_OPT_EPOCH_ITERS (epoch-major order: each warp runs its pieces E iterations at a
+    time, the state through HBM between epochs, next unit's state prefetched): every
+    output of every iteration, split calls, both output transforms, the final state; ragged
+    numrn over several pieces per warp, and numrn with one piece per warp (no prefetch)."""
+    for n, warps in ((70001, 96), (5000, 64)):
+        i = 777
+        want = (oracle.stream_star if out_kind else oracle.stream)(n, i, SEED_PARITY)
+        state = oracle.stream(n, i, SEED_PARITY)[-1]
+        for calls in ([i], [400, 1, 376]):
+            h = P.prng_create(n, SEED_PARITY)
+            try:
+                P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid(kname))
+                P.prng_set_option(h, P.PRNG_OPT_OUTPUT, out_kind)
+                P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, epoch)
+                P.prng_set_option(h, P.PRNG_OPT_TIME_PARALLEL, 0)
+                P.prng_set_option(h, P.PRNG_OPT_GRID_WARPS, warps)
+                out = np.zeros((i, n), np.uint64)
+                sink = P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0)
+                P.prng_init(h)
+                for c in calls:
+                    P.prng_generate(h, c, P.SINK_COPY, sink)
+                st = P.prng_read_state(h, n)
+            finally:
+                P.prng_destroy(h)
+            assert np.array_equal(out, want), (n, calls)
+            assert np.array_equal(st, state)
+
+
+@pytest.mark.parametrize("epoch_opt", [0, -1])
+def test_epoch_auto_device_only_ring(epoch_opt):
+    """Device-only ring of R = 16 slots, 1000 iterations in one launch: the live lines of
+    R slots are far below L2, so the auto rule takes the epoch kernel (E = R); -1 turns it
+    off.  The 16 slots and the final state vs the oracle either way."""
+    n, i, R = 300007, 1000, 16
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, R)
+        P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, epoch_opt)
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        want = oracle.stream(n, i, SEED_PARITY)
+        _, _, _, first, _ = P.prng_device_ring(h)
+        for k in range(i - R, i):
+            assert np.array_equal(P.prng_read_slot(h, (first + k) % R, n), want[k]), k
+        assert np.array_equal(P.prng_read_state(h, n), want[-1])
+    finally:
+        P.prng_destroy(h)
+
+
 def test_forced_chunks_device_only_bench_shape():
     """Forced chunks + CTA-blocked order at the bench width (2^24), device-only into a
     torch buffer: every iteration's XOR and wrapping sum of all 2^24 outputs (folded on the

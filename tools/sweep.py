@@ -48,13 +48,15 @@ def main():
     ap.add_argument("--cta-warps", default="0")
     ap.add_argument("--chunks", default="0", help="PRNG_OPT_CHUNK_ITERS values")
     ap.add_argument("--orders", default="0", help="PRNG_OPT_PIECE_ORDER values")
+    ap.add_argument("--epochs", default="0", help="PRNG_OPT_EPOCH_ITERS values (0 auto, -1 off)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     gen, cop = torch.cuda.Stream(), torch.cuda.Stream()
     vs = range(P.prng_kernel_variants()) if a.variants == "all" else [int(v) for v in a.variants.split(",")]
-    for slots, pad, cw, ch, od in [(int(s), int(p), int(c), int(l), int(o)) for s in a.slots.split(",")
-                                   for p in a.pads.split(",") for c in a.cta_warps.split(",")
-                                   for l in a.chunks.split(",") for o in a.orders.split(",")]:
+    for slots, pad, cw, ch, od, ep in [(int(s), int(p), int(c), int(l), int(o), int(e)) for s in a.slots.split(",")
+                                       for p in a.pads.split(",") for c in a.cta_warps.split(",")
+                                       for l in a.chunks.split(",") for o in a.orders.split(",")
+                                       for e in a.epochs.split(",")]:
         for w in [int(x) for x in a.warps.split(",")]:
             for v in vs:
                 h = P.prng_create(a.numrn, 0)
@@ -66,11 +68,12 @@ def main():
                 P.prng_set_option(h, P.PRNG_OPT_CTA_WARPS, cw)
                 P.prng_set_option(h, P.PRNG_OPT_CHUNK_ITERS, ch)
                 P.prng_set_option(h, P.PRNG_OPT_PIECE_ORDER, od)
+                P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, ep)
                 best, med = run(h, a.numrn, a.numiter, a.reps, gen)
                 _, _, rs, _, _ = P.prng_device_ring(h)
                 P.prng_destroy(h)
                 print(json.dumps({"variant": P.prng_kernel_variant_name(v), "grid_warps": w, "slots": rs, "pad": pad, "cta_warps": cw,
-                                  "numrn": a.numrn, "numiter": a.numiter, "chunk": ch, "order": od,
+                                  "numrn": a.numrn, "numiter": a.numiter, "chunk": ch, "order": od, "epoch": ep,
                                   "best_gbs": round(best, 1), "median_gbs": round(med, 1)}), flush=True)
 
 
