@@ -331,9 +331,14 @@ def run_ours(a, D):
     kmean = statistics.mean(kern_ms)
     algo_bytes = 8 * cnt * a.numiter
     achieved = algo_bytes / (kmean * 1e-3) / 1e9
-    traffic, _ = ncu_traffic()
+    traffic, traffic_algo = ncu_traffic()
+    if traffic_algo is not None and int(traffic_algo) != algo_bytes:
+        traffic = None  # the committed capture is of another shape
+    ran, epoch = P.prng_last_launch(h)  # the kernel the timed launches ran (anti-absorption rule)
+    kname = ("prngk::batch_kernel_epoch<" + P.prng_kernel_variant_name(ran) + f", E={epoch}>" if epoch else
+             "prngk::batch_kernel<" + P.prng_kernel_variant_name(ran) + ">")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "prngk::batch_kernel<" + P.prng_kernel_variant_name(kernel) + ">",
+                "traffic": traffic, "kernel": kname,
                 "grid_warps": grid_warps or "variant default", "autotune_probe_gbs": tune_gbs,
                 "algorithmic_bytes_per_launch": algo_bytes, "mean_launch_ms": kmean,
                 "kernel_share_of_step": sum(kern_ms) / ms, "init_kernel_mean_ms": statistics.mean(init_ms),

@@ -164,7 +164,8 @@ enum prng_option {
                                   1 = state * 0x2545F4914F6CDD1D mod 2^64 (xorshift64*-style
                                   scrambler, A19).  Needs a CTA-synchronised variant with
                                   a scrambled instantiation (v4n4s1, v2n8s1, v2n16s1,
-                                  v4n8s1, v2n4s1); others give PRNG_EINVAL.            */
+                                  v4n8s1, v2n4s1, v4n16s1, v2n32s1); others give
+                                  PRNG_EINVAL.                                         */
     PRNG_OPT_TIME_PARALLEL = 11, /* 1 (default): when numrn is too small to fill the GPU, cut
                                   a launch's iterations into chunks started by GF(2)
                                   jump-ahead (xs^k is linear: a 64x64 bit matrix); 0: off */
@@ -222,6 +223,12 @@ int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t 
  * numbers per thread, free-running warps).  NULL for an id out of range. */
 int prng_kernel_variants(void);
 const char *prng_kernel_variant_name(int id);
+
+/* The batch kernel the handle's last launch actually ran: *variant = its variant id (the
+ * PRNG_OPT_KERNEL choice, or the wider variant the anti-absorption rule substituted for the
+ * default), *epoch_iters = its epoch length (0 = natural order).  -1 / 0
+ * before any launch.  Either pointer may be NULL.  PRNG_EINVAL for a NULL handle. */
+int prng_last_launch(const prng_t *h, int *variant, uint32_t *epoch_iters, prng_err_t *err);
 
 /* ------------------------------------------------------------------ profiling (a6) */
 /* Event name ids, as cf4ocl names them in Fig. 3 plus the host sink. */

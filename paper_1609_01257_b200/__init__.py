@@ -19,7 +19,7 @@ __all__ = [
     "prng_generate", "prng_generate_device", "prng_generate_host", "prng_seek", "prng_device_ring", "prng_read_slot",
     "prng_read_state", "prng_set_option", "prng_get_option", "prng_set_streams",
     "prng_strerror", "prng_prof_events", "prng_prof_calc", "prng_event_name",
-    "prng_kernel_variants", "prng_kernel_variant_name", "prng_autotune", "prng_probe_memset_gbs",
+    "prng_kernel_variants", "prng_kernel_variant_name", "prng_last_launch", "prng_autotune", "prng_probe_memset_gbs",
     "prng_probe_store_gbs", "prng_probe_d2h_gbs", "SINK_NULL", "SINK_COPY", "SINK_DIGEST",
     "CopySink", "DigestSink", "SINK_FN",
     "PRNG_OPT_MODE", "PRNG_OPT_BATCH_ITERS", "PRNG_OPT_RING_SLOTS", "PRNG_OPT_PROFILE",
@@ -98,6 +98,7 @@ def lib():
         "prng_autotune": ([vp, u64, PD, E], i32),
         "prng_kernel_variants": ([], i32),
         "prng_kernel_variant_name": ([i32], ctypes.c_char_p),
+        "prng_last_launch": ([vp, ctypes.POINTER(i32), P32, E], i32),
         "prng_event_name": ([u32], ctypes.c_char_p),
         "prng_prof_events": ([vp, u64, vp, vp, vp, P64, PD, E], i32),
         "prng_prof_calc": ([u64, vp, vp, vp, u32, dbl, vp, vp, PD, PD, E], i32),
@@ -278,6 +279,14 @@ def prng_kernel_variants() -> int:
 def prng_kernel_variant_name(i: int) -> str:
     r = lib().prng_kernel_variant_name(i)
     return r.decode() if r else None
+
+
+def prng_last_launch(h):
+    """(variant id, epoch iterations) of the handle's last batch launch."""
+    err = prng_err_t()
+    v, e = ctypes.c_int(-1), ctypes.c_uint32(0)
+    _check(lib().prng_last_launch(h, ctypes.byref(v), ctypes.byref(e), ctypes.byref(err)), err)
+    return v.value, e.value
 
 
 def prng_event_name(i: int) -> str:

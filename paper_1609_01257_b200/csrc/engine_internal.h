@@ -98,6 +98,8 @@ struct prng {
     int64_t chunk_iters = 0;  // PRNG_OPT_CHUNK_ITERS
     int piece_order = 0;      // PRNG_OPT_PIECE_ORDER
     int64_t epoch_iters = 0;  // PRNG_OPT_EPOCH_ITERS
+    int last_kernel = -1;     // variant id of the last batch launch (after the anti-absorption rule)
+    uint32_t last_epoch = 0;  // its epoch length (0: natural order)
     unsigned long long *trace = nullptr;  // PRNG_OPT_TRACE_PTR (diagnostic variant only)
 
     int profile = 0, kernel = 0, output = 0, blocking = 1;

@@ -66,9 +66,9 @@ const Variant kVariants[] = {
     V("v2n8c2", 2, 8, 0, 2, 2, 4),    V("v2n8c4", 2, 8, 0, 2, 4, 4),
     // long per-CTA chunks: 32 / 64 numbers per thread (16 / 32 KiB per warp per iteration)
     // (measured: no gain over v2n4s1; 64 numbers/thread spills and was removed)
-    V("v2n32s1", 2, 32, 0, 1, 1, 4),  V("v4n32s1", 4, 32, 0, 1, 1, 4),
+    VS("v2n32s1", 2, 32, 4),  V("v4n32s1", 4, 32, 0, 1, 1, 4),
     // fewer instructions per number (32-B stores, more numbers per thread): less SM power
-    V("v4n12s1", 4, 12, 0, 1, 1, 4),  V("v4n16s1", 4, 16, 0, 1, 1, 4),
+    V("v4n12s1", 4, 12, 0, 1, 1, 4),  VS("v4n16s1", 4, 16, 4),
     // store cache policies on the default structure: .cs, L2::evict_first, L1::no_allocate
     V("v2n4s1cs", 2, 4, 1, 1, 1, 4),  V("v2n4s1ef", 2, 4, 2, 1, 1, 4), V("v2n4s1na", 2, 4, 3, 1, 1, 4),
     // diagnostic: v2n4s1 + per-CTA %globaltimer trace (PRNG_OPT_TRACE_PTR)
@@ -159,10 +159,58 @@ int prof_end(prng *h, cudaStream_t s, prng_err_t *err) {
     return PRNG_OK;
 }
 
+// Persistent grid of a variant: at most one wave of resident warps.
+static uint64_t max_grid_warps(const prng *h, int vid) {
+    const Variant &v = kVariants[vid];
+    uint64_t w = (uint64_t)h->blocks_per_sm[vid] * h->num_sms * (kBlock / 32);
+    if (h->grid_warps > 0)
+        w = std::min<uint64_t>(w, (uint64_t)h->grid_warps);
+    else if (v.warps_per_sm > 0)
+        w = std::min<uint64_t>(w, (uint64_t)v.warps_per_sm * h->num_sms);
+    return std::max<uint64_t>(w, kBlock / 32);
+}
+
+// L2 absorption (profiles/r1_l2_absorption.md): in the natural order a warp
+// runs one piece through all of a launch's iterations, so when the launch wraps a ring of
+// R slots it rewrites the same R x (bytes per warp-iteration) every R iterations.  While
+// the grid's live set -- R x warps x bytes per warp-iteration -- fits in L2, the rewrites
+// hit dirty L2 lines and never reach DRAM (ncu: 12 % of the stores reach DRAM at
+// numrn = 2^27 through 64 slots).  That is not sustained output bandwidth, so such launches
+// are reorganised: a variant with more numbers per warp-iteration, or epoch order.
+static uint64_t live_bytes(const prng *h, int vid, uint64_t nslots) {
+    const uint64_t piece = 32ull * kVariants[vid].npt;
+    const uint64_t npieces = (h->count + piece - 1) / piece;
+    return nslots * std::min<uint64_t>(max_grid_warps(h, vid), npieces) * piece * sizeof(uint64_t);
+}
+static bool absorbs(const prng *h, int vid, uint64_t nslots, uint32_t iters) {
+    return iters > nslots && live_bytes(h, vid, nslots) < 2 * (uint64_t)h->l2_bytes;
+}
+// Default-variant substitutes in order of numbers per warp-iteration (2, 4, 8 KiB):
+// same CTA-synchronised 4-warps-per-SM structure as v4n4s1.
+static const char *const kWideNames[] = {"v4n8s1", "v4n16s1", "v2n32s1"};
+
+static int variant_id(const char *name) {
+    for (int i = 0; i < kNumVariants; ++i)
+        if (!std::strcmp(kVariants[i].name, name)) return i;
+    return -1;
+}
+
 // Launch one batch of `iters` iterations (a2 + a3) into dst slots.
 int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64_t slot0, uint32_t iters,
                  bool first_is_state, cudaStream_t s, prng_err_t *err) {
-    const Variant &v0 = kVariants[h->kernel];
+    int vid = h->kernel;
+    // Anti-absorption, first choice: the default variant is swapped for the narrowest wide
+    // one whose live set exceeds 2x L2 (output identical; measured honest and as fast).
+    if (vid == 0 && h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 && absorbs(h, 0, nslots, iters)) {
+        for (const char *nm : kWideNames) {
+            const int w = variant_id(nm);
+            if (w >= 0 && !absorbs(h, w, nslots, iters)) {
+                vid = w;
+                break;
+            }
+        }
+    }
+    const Variant &v0 = kVariants[vid];
     Variant v = v0;
     if (h->output == 1) {
         if (!v0.star) return set_err(err, PRNG_EINVAL, "output scrambling not compiled for variant %s", v0.name);
@@ -187,12 +235,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     const uint64_t piece = 32ull * v.npt;
     a.npieces = (h->count + piece - 1) / piece;
     // Persistent grid: at most one wave of resident warps; equalise pieces per warp.
-    uint64_t max_warps = (uint64_t)h->blocks_per_sm[h->kernel] * h->num_sms * (kBlock / 32);
-    if (h->grid_warps > 0)
-        max_warps = std::min<uint64_t>(max_warps, (uint64_t)h->grid_warps);
-    else if (v.warps_per_sm > 0)
-        max_warps = std::min<uint64_t>(max_warps, (uint64_t)v.warps_per_sm * h->num_sms);
-    max_warps = std::max<uint64_t>(max_warps, kBlock / 32);
+    const uint64_t max_warps = max_grid_warps(h, vid);
     // Time-parallel mode (NEXT-4): when the pieces cannot fill the grid (small numrn), cut
     // the launch's iterations into chunks started by GF(2) jump-ahead, so that
     // pieces x chunks units fill it.
@@ -203,17 +246,13 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
         nch = (iters + h->chunk_iters - 1) / h->chunk_iters;  // PRNG_OPT_CHUNK_ITERS: forced
     else if (h->time_parallel && v.stages == 0 && 2 * a.npieces <= max_warps && iters >= 512)
         nch = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
-    // Epoch-major order (batch_kernel_epoch, DESIGN.md §5 "L2 absorption"): when a launch
-    // wraps the ring and the natural order would rewrite an address while its line can
-    // still be in L2 (the grid rewrites its pieces' R slots every R iterations: R x warps x
-    // bytes per warp-iteration of live lines), cut the launch into epochs of E = R
-    // iterations, so an address is rewritten only one whole epoch (the full ring) later.
+    // Anti-absorption, fallback: epoch-major order (batch_kernel_epoch) with E = R, so an
+    // address is rewritten only one whole epoch (the full ring) later.
     uint64_t E = 0;
     if (v.epoch && nch <= 1 && h->epoch_iters >= 0) {
-        const uint64_t live = nslots * std::min<uint64_t>(max_warps, a.npieces) * piece * sizeof(uint64_t);
         if (h->epoch_iters > 0)
             E = (uint64_t)h->epoch_iters;  // PRNG_OPT_EPOCH_ITERS: forced
-        else if (iters > nslots && live < 2 * (uint64_t)h->l2_bytes)
+        else if (absorbs(h, vid, nslots, iters))
             E = nslots;
         if (E >= iters) E = 0;
     }
@@ -274,6 +313,8 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
         blocks = std::min<uint64_t>((blocks + C - 1) / C, (uint64_t)max_cl) * C;
     }
     a.rounds = (uint32_t)((units + blocks * wpb - 1) / (blocks * wpb));
+    h->last_kernel = vid;
+    h->last_epoch = (uint32_t)E;
     if (int rc = prof_begin(h, s, PRNG_EV_RNG_KERNEL, err)) return rc;
     if (C > 1) {
         cudaLaunchConfig_t cfg = {};
@@ -331,6 +372,12 @@ const char *prng_event_name(uint32_t id) {
 }
 
 int prng_kernel_variants(void) { return kNumVariants; }
+int prng_last_launch(const prng_t *h, int *variant, uint32_t *epoch_iters, prng_err_t *err) {
+    if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
+    if (variant) *variant = h->last_kernel;
+    if (epoch_iters) *epoch_iters = h->last_epoch;
+    return ok(err);
+}
 const char *prng_kernel_variant_name(int id) { return (id >= 0 && id < kNumVariants) ? kVariants[id].name : nullptr; }
 
 prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begin, uint64_t gid_count,

@@ -446,34 +446,33 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
 }
 
 // ---------------------------------------------------------------- a2+a3, epoch-major order
-// Measured (profiles/r1_sweeps.md, "Concurrently written slots"): the write stream slows
-// down when the grid writes into many ring slots (= iterations) at once.  batch_kernel
-// runs each piece through all T iterations of the launch; the CTAs drift apart by ~180
-// iterations, so ~148 slots are written concurrently.  Here the launch is cut into epochs
-// of E iterations: in epoch e every warp runs each of its pieces (piece r*W + w, r =
-// 0, 1, ...) through iterations [eE, eE + E), keeping the state in registers inside an
-// epoch and in d_state between epochs.  Only the <= E slots of the current epoch (two at
-// an epoch boundary) are being written.  Extra traffic: 16 B per number per epoch
-// (2/E of the output).
+// L2 absorption: batch_kernel runs each piece through all T iterations of a
+// launch, so when a launch wraps a ring of R slots a warp rewrites its piece's R slots
+// every R iterations; if the grid's live set (R x warps x bytes per warp-iteration) fits
+// in L2 the rewrites merge in L2 and never reach DRAM.  Here the launch is cut into epochs
+// of E <= R iterations: in epoch e every warp runs each of its pieces (piece r*W + w,
+// r = 0, 1, ...) through iterations [eE, eE + E), keeping the state in registers inside a
+// unit and in d_state between epochs, so an address is rewritten only a whole epoch (all
+// pieces x E iterations) later.  Extra traffic: 16 B per number per epoch (2/E of the
+// output).
 //
-// Every piece of a warp is always run by the same lanes, so a state written at the end
-// of one unit is read back by the thread that wrote it (program order; no grid sync).
-// The next unit's state is prefetched while the current unit runs (a load issued behind
-// a saturated write stream takes ~1 us), which needs >= 2 pieces per warp (the host
-// checks npieces >= 2 W); the load is .cg, as the state is rewritten during the launch.
-// CTA barrier every iteration as in SYNC 1.
-__device__ __forceinline__ void ld_v4_cg(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
-    asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+// Every piece of a warp is always run by the same lanes, so a state written at the end of
+// one unit is read back by the thread that wrote it: a weak load is enough (same-thread
+// program order, PTX memory model) -- and measured faster than a .cg (LDG.STRONG.GPU)
+// load or prefetching the next unit's state during the current one (exp21).  CTA barrier
+// every iteration as in SYNC 1.
+__device__ __forceinline__ void ld_v4_wk(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
+    asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
 }
-__device__ __forceinline__ void ld_v2_cg(const uint64_t *p, uint64_t &a, uint64_t &b) {
-    asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+__device__ __forceinline__ void ld_v2_wk(const uint64_t *p, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
 }
 template <int VEC>
-__device__ __forceinline__ void load_vec_cg(const uint64_t *p, uint64_t *x) {
+__device__ __forceinline__ void load_vec_wk(const uint64_t *p, uint64_t *x) {
     if constexpr (VEC == 4)
-        ld_v4_cg(p, x[0], x[1], x[2], x[3]);
+        ld_v4_wk(p, x[0], x[1], x[2], x[3]);
     else
-        ld_v2_cg(p, x[0], x[1]);
+        ld_v2_wk(p, x[0], x[1]);
 }
 
 // One unit of the epoch kernel: a piece through iterations [t_begin, t_begin + t_count).
@@ -537,16 +536,7 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
     // rounds (or epochs) on the same named barrier.
     const uint64_t kw_cta = (a.npieces - cta_warp0 + nwarps - 1) / nwarps;
     const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - cta_warp0 < wpb ? a.npieces - cta_warp0 : wpb);
-    const bool prefetch = kw >= 2;  // kw == 1: the next unit is this piece again (not written yet)
     const uint32_t E = a.chunk_len;
-    auto is_full = [&](uint64_t piece) { return (piece + 1) * PIECE <= a.count; };
-    auto lane_base = [&](uint64_t piece) { return piece * PIECE + (uint64_t)lane * VEC; };
-    auto load_full = [&](uint64_t piece, uint64_t *dst) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) load_vec_cg<VEC>(a.state + lane_base(piece) + (uint64_t)v * 32 * VEC, dst + v * VEC);
-    };
-    uint64_t xn[NPT];  // prefetched state of the next unit (full pieces)
-    if (prefetch && is_full(warp)) load_full(warp, xn);
     for (uint32_t e = 0; e < a.nchunks; ++e) {
         const uint32_t t_begin = e * E;
         const uint32_t t_count = a.iters - t_begin < E ? a.iters - t_begin : E;
@@ -558,32 +548,22 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
                 continue;
             }
             const uint64_t piece = r * nwarps + warp;
-            const uint64_t base = lane_base(piece);
+            const uint64_t base = piece * PIECE + (uint64_t)lane * VEC;
             uint64_t x[NPT];
-            if (is_full(piece)) {
-                if (prefetch) {
+            if ((piece + 1) * PIECE <= a.count) {
 #pragma unroll
-                    for (int j = 0; j < NPT; ++j) x[j] = xn[j];
-                    // the next unit: the next piece of this epoch, or the warp's first piece of
-                    // the next epoch (its state was written at the end of this epoch's unit 0)
-                    const uint64_t np = r + 1 < kw ? piece + nwarps : warp;
-                    if ((r + 1 < kw || e + 1 < a.nchunks) && is_full(np)) load_full(np, xn);
-                } else {
-                    load_full(piece, x);
-                }
+                for (int v = 0; v < NV; ++v) load_vec_wk<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
                 epoch_unit<VEC, NPT, OUT, true>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
-            } else {  // the ragged last piece (its successor, if any, is never a full piece of
-                      // a later round: it is the last piece)
+            } else {  // the ragged last piece
 #pragma unroll
                 for (int v = 0; v < NV; ++v)
 #pragma unroll
                     for (int q = 0; q < VEC; ++q) {
                         const uint64_t idx = base + (uint64_t)v * 32 * VEC + q;
-                        x[v * VEC + q] = idx < a.count ? __ldcg(a.state + idx) : 0ull;
+                        x[v * VEC + q] = idx < a.count ? a.state[idx] : 0ull;
                     }
-                if (prefetch && e + 1 < a.nchunks && is_full(warp)) load_full(warp, xn);
                 epoch_unit<VEC, NPT, OUT, false>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
 #pragma unroll
                 for (int v = 0; v < NV; ++v)

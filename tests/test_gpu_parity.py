@@ -10,7 +10,7 @@ import paper_1609_01257_b200 as P
 from workloads import RAGGED_N, SEED_PARITY, SPEC_GRID_I, SPEC_GRID_N, sample_points, shard_range
 
 # variants compiled with the NEXT-3 scrambled-output instantiation (prng_engine.cu VS(...))
-STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1")
+STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1", "v4n16s1", "v2n32s1")
 
 
 def _kid(name):
@@ -491,23 +491,53 @@ def test_epoch_order(kname, epoch, out_kind):
             assert np.array_equal(st, state)
 
 
-@pytest.mark.parametrize("epoch_opt", [0, -1])
-def test_epoch_auto_device_only_ring(epoch_opt):
-    """Device-only ring of R = 16 slots, 1000 iterations in one launch: the live lines of
-    R slots are far below L2, so the auto rule takes the epoch kernel (E = R); -1 turns it
-    off.  The 16 slots and the final state vs the oracle either way."""
-    n, i, R = 300007, 1000, 16
+# (numrn, iterations, ring slots, epoch option, expected (variant, epoch length)); L2 = 126 MB
+# on B200, 592 warps: live set = R x min(592, pieces) x bytes per warp-iteration vs 2 x L2.
+ANTI_ABSORPTION = [
+    (300007, 1000, 16, 0, ("v4n4s1", 16)),   # no wide variant clears 2 x L2: epoch order, E = R
+    (300007, 1000, 16, -1, ("v4n4s1", 0)),   # -1: natural order (absorbing) on request
+    (300007, 40, 64, 0, ("v4n4s1", 0)),      # no wrap inside the launch: nothing to absorb
+    (1 << 20, 200, 64, 0, ("v2n32s1", 0)),   # 64 x 592 x 8 KiB = 310 MB: the 8 KiB variant
+    (1 << 20, 400, 300, 0, ("v4n8s1", 0)),   # 300 x 592 x 2 KiB = 364 MB: the 2 KiB variant
+    ((1 << 20) + 77, 200, 64, 0, ("v2n32s1", 0)),  # ragged
+]
+
+
+@pytest.mark.parametrize("n,i,R,epoch_opt,expect", ANTI_ABSORPTION)
+@pytest.mark.parametrize("out_kind", [0, 1])
+def test_anti_absorption_rule(n, i, R, epoch_opt, expect, out_kind):
+    """The device-only launch wraps a ring of R slots: the default variant is replaced by a
+    wider one (or epoch order) so that no address is rewritten while its line can still be
+    in L2.  The kernel that ran (prng_last_launch), the R slots still in the
+    ring and the final state vs the oracle."""
     h = P.prng_create(n, SEED_PARITY)
     try:
         P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, R)
         P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, epoch_opt)
+        P.prng_set_option(h, P.PRNG_OPT_OUTPUT, out_kind)
         P.prng_init(h)
         P.prng_generate(h, i)
-        want = oracle.stream(n, i, SEED_PARITY)
+        ran, epoch = P.prng_last_launch(h)
+        assert (P.prng_kernel_variant_name(ran), epoch) == expect
+        want = (oracle.stream_star if out_kind else oracle.stream)(n, i, SEED_PARITY)
         _, _, _, first, _ = P.prng_device_ring(h)
-        for k in range(i - R, i):
+        for k in range(max(0, i - R), i):
             assert np.array_equal(P.prng_read_slot(h, (first + k) % R, n), want[k]), k
-        assert np.array_equal(P.prng_read_state(h, n), want[-1])
+        assert np.array_equal(P.prng_read_state(h, n), oracle.stream(n, i, SEED_PARITY)[-1])
+    finally:
+        P.prng_destroy(h)
+
+
+def test_bench_shape_keeps_default_kernel():
+    """numrn = 2^24 x 1000 through the default 64 GiB ring (512 slots): 512 x 592 x 1 KiB =
+    310 MB > 2 x L2, so the bench launch runs v4n4s1 in natural order."""
+    h = P.prng_create(1 << 24, 0)
+    try:
+        P.prng_init(h)
+        P.prng_generate(h, 1000)
+        _, _, slots, _, _ = P.prng_device_ring(h)
+        assert slots == 512
+        assert P.prng_last_launch(h) == (0, 0)
     finally:
         P.prng_destroy(h)
 

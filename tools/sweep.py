@@ -71,9 +71,11 @@ def main():
                 P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, ep)
                 best, med = run(h, a.numrn, a.numiter, a.reps, gen)
                 _, _, rs, _, _ = P.prng_device_ring(h)
+                ran, ran_e = P.prng_last_launch(h)
                 P.prng_destroy(h)
                 print(json.dumps({"variant": P.prng_kernel_variant_name(v), "grid_warps": w, "slots": rs, "pad": pad, "cta_warps": cw,
                                   "numrn": a.numrn, "numiter": a.numiter, "chunk": ch, "order": od, "epoch": ep,
+                                  "ran": P.prng_kernel_variant_name(ran), "ran_epoch": ran_e,
                                   "best_gbs": round(best, 1), "median_gbs": round(med, 1)}), flush=True)
 
 
