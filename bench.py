@@ -6,7 +6,7 @@
 
 One "step" = one pass of the whole hot path over one synthetic workload:
 prng_init (a1, seeding kernel) + prng_generate(numiter) (a2+a3: xorshift64 batch kernel,
-register-resident state, 16-byte stores into a device ring).  BASELINE.json's metric is
+register-resident state, 32-byte stores into a device ring).  BASELINE.json's metric is
 random numbers/s (and GB/s, 8 B per number, Eq. 1) device-only and end to end.
 
 * value      device-only numbers/s over all ranks: inputs (numrn, numiter, seed) resident,
@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--numrn-total", type=int, default=0, help="strong scaling: fixed total numrn (e.g. 2^28)")
     ap.add_argument("--numiter", type=int, default=DEF_NUMITER)
     ap.add_argument("--seed", type=int, default=SEED_PERF)
-    ap.add_argument("--kernel", type=int, default=0, help="kernel variant id (default 0 = v4n4s1; -1: prng_autotune)")
+    ap.add_argument("--kernel", type=int, default=0, help="kernel variant id (default 0 = auto: v4n8s1 at the bench shape; -1: prng_autotune)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--e2e-mode", type=int, default=3, help="0 S0, 1 S1, 2 O1, 3 O2, 4 O3 (zero-copy)")
@@ -197,13 +197,19 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the batch kernel from the committed ncu --set full summary."""
+def ncu_traffic(variant, epoch):
+    """Per-launch DRAM bytes of the batch kernel from the committed ncu --set full summary,
+    if that capture is of this kernel (variant "v{VEC}n{NPT}s1", natural order)."""
+    import re
     p = os.path.join(ROOT, "profiles", "ncu_batch_kernel.json")
-    if not os.path.exists(p):
+    m = re.fullmatch(r"v(\d+)n(\d+)s1", variant or "")
+    if not os.path.exists(p) or not m or epoch:
         return None, None
     with open(p) as f:
         d = json.load(f)
+    want = f"batch_kernel<{m.group(1)}, {m.group(2)}, 0, 1, 0>"
+    if not any(want in k.get("kernel", "") for k in d.get("kernels", [])):
+        return None, None
     return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
 
 
@@ -331,10 +337,10 @@ def run_ours(a, D):
     kmean = statistics.mean(kern_ms)
     algo_bytes = 8 * cnt * a.numiter
     achieved = algo_bytes / (kmean * 1e-3) / 1e9
-    traffic, traffic_algo = ncu_traffic()
+    ran, epoch = P.prng_last_launch(h)  # the kernel the timed launches ran ("auto", anti-absorption)
+    traffic, traffic_algo = ncu_traffic(P.prng_kernel_variant_name(ran), epoch)
     if traffic_algo is not None and int(traffic_algo) != algo_bytes:
         traffic = None  # the committed capture is of another shape
-    ran, epoch = P.prng_last_launch(h)  # the kernel the timed launches ran (anti-absorption rule)
     kname = ("prngk::batch_kernel_epoch<" + P.prng_kernel_variant_name(ran) + f", E={epoch}>" if epoch else
              "prngk::batch_kernel<" + P.prng_kernel_variant_name(ran) + ">")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -152,7 +152,10 @@ enum prng_option {
     PRNG_OPT_PROFILE = 4,      /* 1 = record per-batch intervals (CUDA events), reset by
                                   prng_init; 2 = same, accumulated across prng_init calls
                                   and without the host syncs mode 1 adds for wall time    */
-    PRNG_OPT_KERNEL = 5,       /* kernel variant id (see prng_kernel_variants); 0 = default */
+    PRNG_OPT_KERNEL = 5,       /* kernel variant id (see prng_kernel_variants); 0 = "auto"
+                                  (default): v4n8s1 from 2^21 work-items per handle, v4n4s1
+                                  below, widened / epoch-ordered by the anti-absorption rule
+                                  (see PRNG_OPT_EPOCH_ITERS, prng_last_launch)            */
     PRNG_OPT_GRID_WARPS = 6,   /* cap on resident warps of the persistent grid; 0 = auto  */
     PRNG_OPT_RING_PAD = 7,     /* extra u64 elements between device-only ring slots (multiple
                                   of 4; breaks power-of-two slot strides); default 0       */
@@ -217,10 +220,11 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
  * PRNG_ESTATE otherwise).  best_gbs (may be NULL) gets the winner's probe GB/s. */
 int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err);
 
-/* Number of kernel variants compiled in, and the name of one (id 0 "v4n4s1", the default:
- * one 32-byte store per thread per iteration, 4 numbers per thread, CTA barrier every
- * iteration; "v2n4s1" = the same with two 16-byte stores; "v4n8" = 32-byte stores, 8
- * numbers per thread, free-running warps).  NULL for an id out of range. */
+/* Number of kernel variants compiled in, and the name of one (id 0 "auto", the default,
+ * resolved per launch -- see PRNG_OPT_KERNEL; "v4n4s1" = one 32-byte store per thread per
+ * iteration, 4 numbers per thread, CTA barrier every iteration; "v4n8s1" = the same with 8
+ * numbers per thread; "v2n4s1" = two 16-byte stores; "v4n8" = 32-byte stores, 8 numbers
+ * per thread, free-running warps).  NULL for an id out of range. */
 int prng_kernel_variants(void);
 const char *prng_kernel_variant_name(int id);
 

@@ -55,8 +55,10 @@ struct Variant {
 // ~2 % ahead of two 16-B ones, 7.29 TB/s at numrn = 2^27); free-running warps at full
 // occupancy ~6.2 TB/s (more concurrently open DRAM pages).
 const Variant kVariants[] = {
-    VS("v4n4s1", 4, 4, 4),  // default: one 32-B store per thread per iteration, 4 numbers/thread,
-                            // CTA barrier, 4 warps/SM (round-1 default v2n4s1 is id 28)
+    // id 0 "auto" (the default): resolved per launch by launch_batch -- v4n8s1 at >= 2^21
+    // work-items per handle, v4n4s1 below (measured), then widened or run in
+    // epoch order by the anti-absorption rule.  Its own fields (= v4n4s1) size the grid.
+    VS("auto", 4, 4, 4),
     VS("v2n8s1", 2, 8, 4),  VS("v2n16s1", 2, 16, 4), VS("v4n8s1", 4, 8, 4),
     // free-running warps
     V("v4n8", 4, 8, 0, 0, 1, 0),      V("v2n4", 2, 4, 0, 0, 1, 0),     V("v2n8", 2, 8, 0, 0, 1, 0),
@@ -78,6 +80,9 @@ const Variant kVariants[] = {
     VT("t2n4w8", 4, 4, 8), VT("t2n8w8", 8, 4, 8),
     // the round-1 default: two 16-B stores per thread per iteration (r1_sweeps.md "32-B stores")
     VS("v2n4s1", 2, 4, 4),
+    // one 32-B store per thread per iteration, 4 numbers/thread, CTA barrier, 4 warps/SM:
+    // the default until session 2 of round 1 (now "auto" below 2^21 work-items)
+    VS("v4n4s1", 4, 4, 4),
 };
 #undef VT
 #undef VS
@@ -188,6 +193,11 @@ static bool absorbs(const prng *h, int vid, uint64_t nslots, uint32_t iters) {
 // Default-variant substitutes in order of numbers per warp-iteration (2, 4, 8 KiB):
 // same CTA-synchronised 4-warps-per-SM structure as v4n4s1.
 static const char *const kWideNames[] = {"v4n8s1", "v4n16s1", "v2n32s1"};
+// "auto": one 32-B store per thread per iteration and a CTA barrier, 8 numbers per thread
+// (2 KiB per warp-iteration) from this many work-items per handle, 4 below.  Measured on
+// B200 (profiles/r1_sweeps.md, "Default"): v4n8s1 writes 7-9 % faster than v4n4s1 at
+// 2^21..2^24 on some boxes and ties on others; v4n4s1 is ahead at 2^18 and 2^20.
+constexpr uint64_t kAutoWideFrom = 1ull << 21;
 
 static int variant_id(const char *name) {
     for (int i = 0; i < kNumVariants; ++i)
@@ -199,14 +209,18 @@ static int variant_id(const char *name) {
 int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64_t slot0, uint32_t iters,
                  bool first_is_state, cudaStream_t s, prng_err_t *err) {
     int vid = h->kernel;
-    // Anti-absorption, first choice: the default variant is swapped for the narrowest wide
-    // one whose live set exceeds 2x L2 (output identical; measured honest and as fast).
-    if (vid == 0 && h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 && absorbs(h, 0, nslots, iters)) {
-        for (const char *nm : kWideNames) {
-            const int w = variant_id(nm);
-            if (w >= 0 && !absorbs(h, w, nslots, iters)) {
-                vid = w;
-                break;
+    if (vid == 0) {  // "auto"
+        vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1" : "v4n4s1");
+        // Anti-absorption, first choice: the narrowest wider variant whose live set exceeds
+        // 2x L2 (output identical; measured honest and as fast).  Not with a user grid.
+        if (h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 && absorbs(h, vid, nslots, iters)) {
+            for (const char *nm : kWideNames) {
+                const int w = variant_id(nm);
+                if (kVariants[w].npt * kVariants[w].vec > kVariants[vid].npt * kVariants[vid].vec &&
+                    !absorbs(h, w, nslots, iters)) {
+                    vid = w;
+                    break;
+                }
             }
         }
     }
@@ -761,6 +775,9 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
     if (int rc = ensure_ring(h, 0, err)) return rc;
     if (probe_iters == 0)  // ~16 GiB of output per probe, within [8, 1000] iterations
         probe_iters = std::min<uint64_t>(1000, std::max<uint64_t>(8, (16ull << 30) / (h->count * 8)));
+    // a probe never wraps the ring inside its launch: no rewrite can be absorbed in L2
+    // (DESIGN.md §5), so every candidate is timed on DRAM-bound stores
+    probe_iters = std::min<uint64_t>(probe_iters, h->ring_slots);
     const int saved_profile = h->profile;
     h->profile = 0;
     cudaEvent_t e0, e1;

@@ -528,16 +528,26 @@ def test_anti_absorption_rule(n, i, R, epoch_opt, expect, out_kind):
         P.prng_destroy(h)
 
 
-def test_bench_shape_keeps_default_kernel():
-    """numrn = 2^24 x 1000 through the default 64 GiB ring (512 slots): 512 x 592 x 1 KiB =
-    310 MB > 2 x L2, so the bench launch runs v4n4s1 in natural order."""
-    h = P.prng_create(1 << 24, 0)
+@pytest.mark.parametrize("n,name", [(1 << 24, "v4n8s1"), ((1 << 21) - 1, "v4n4s1"), (1 << 21, "v4n8s1")])
+def test_auto_kernel_at_bench_shape(n, name):
+    """"auto" (id 0): v4n8s1 from 2^21 work-items, v4n4s1 below.  At the bench shape
+    (2^24 x 1000, default 64 GiB ring = 512 slots) the live set is 512 x 592 x 2 KiB =
+    620 MB > 2 x L2, so v4n8s1 runs in natural order; the last iteration and the state vs
+    the oracle (sampled gids)."""
+    h = P.prng_create(n, SEED_PARITY)
     try:
         P.prng_init(h)
         P.prng_generate(h, 1000)
-        _, _, slots, _, _ = P.prng_device_ring(h)
-        assert slots == 512
-        assert P.prng_last_launch(h) == (0, 0)
+        base, pitch, slots, first, end = P.prng_device_ring(h)
+        ran, epoch = P.prng_last_launch(h)
+        assert (P.prng_kernel_variant_name(ran), epoch) == (name, 0)
+        if n == 1 << 24:
+            assert slots == 512
+        last = P.prng_read_slot(h, (first + 999) % slots, n)
+        g = np.random.default_rng(5).integers(0, n, 2000)
+        want = np.array([oracle.sample(int(x), 999, SEED_PARITY) for x in g], dtype=np.uint64)
+        assert np.array_equal(last[g], want)
+        assert np.array_equal(P.prng_read_state(h, n)[g], want)
     finally:
         P.prng_destroy(h)
 
