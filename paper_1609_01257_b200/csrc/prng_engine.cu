@@ -214,13 +214,24 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
         // Anti-absorption, first choice: the narrowest wider variant whose live set exceeds
         // 2x L2 (output identical; measured honest and as fast).  Not with a user grid.
         if (h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 && absorbs(h, vid, nslots, iters)) {
+            int widest = vid;
+            bool found = false;
             for (const char *nm : kWideNames) {
                 const int w = variant_id(nm);
-                if (kVariants[w].npt * kVariants[w].vec > kVariants[vid].npt * kVariants[vid].vec &&
-                    !absorbs(h, w, nslots, iters)) {
+                if (kVariants[w].npt * kVariants[w].vec <= kVariants[vid].npt * kVariants[vid].vec) continue;
+                widest = w;
+                if (!absorbs(h, w, nslots, iters)) {
                     vid = w;
+                    found = true;
                     break;
                 }
+            }
+            // none clears 2x L2: epoch order below, on the widest variant (fewest units,
+            // so the per-unit state round trip is amortised over the most stores) if it
+            // still has a piece for every warp of the grid
+            if (!found) {
+                const uint64_t wp = 32ull * kVariants[widest].npt;
+                if ((h->count + wp - 1) / wp >= max_grid_warps(h, widest)) vid = widest;
             }
         }
     }
@@ -255,11 +266,16 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // pieces x chunks units fill it.
     uint64_t units = a.npieces;
     // (chunks >= 256 iterations keep the per-unit 64-step mat-vec below ~10 % of its work)
+    // Chunks of one piece run concurrently on different warps, so they are only used when
+    // the launch does not wrap its slots (iters <= nslots): otherwise two chunks could
+    // write the same slot and the earlier iteration could land last.
     uint64_t nch = 0;
-    if (v.stages == 0 && h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters)
-        nch = (iters + h->chunk_iters - 1) / h->chunk_iters;  // PRNG_OPT_CHUNK_ITERS: forced
-    else if (h->time_parallel && v.stages == 0 && 2 * a.npieces <= max_warps && iters >= 512)
-        nch = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
+    if (iters <= nslots) {
+        if (v.stages == 0 && h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters)
+            nch = (iters + h->chunk_iters - 1) / h->chunk_iters;  // PRNG_OPT_CHUNK_ITERS: forced
+        else if (h->time_parallel && v.stages == 0 && 2 * a.npieces <= max_warps && iters >= 512)
+            nch = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
+    }
     // Anti-absorption, fallback: epoch-major order (batch_kernel_epoch) with E = R, so an
     // address is rewritten only one whole epoch (the full ring) later.
     uint64_t E = 0;
