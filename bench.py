@@ -199,15 +199,15 @@ def measured_peaks():
 
 def ncu_traffic(variant, epoch):
     """Per-launch DRAM bytes of the batch kernel from the committed ncu --set full summary,
-    if that capture is of this kernel (variant "v{VEC}n{NPT}s1", natural order)."""
+    if that capture is of this kernel (variant "v{VEC}n{NPT}s1[a]", natural order)."""
     import re
     p = os.path.join(ROOT, "profiles", "ncu_batch_kernel.json")
-    m = re.fullmatch(r"v(\d+)n(\d+)s1", variant or "")
+    m = re.fullmatch(r"v(\d+)n(\d+)s1(a?)", variant or "")
     if not os.path.exists(p) or not m or epoch:
         return None, None
     with open(p) as f:
         d = json.load(f)
-    want = f"batch_kernel<{m.group(1)}, {m.group(2)}, 0, 1, 0>"
+    want = f"batch_kernel<{m.group(1)}, {m.group(2)}, 0, 1, 0, {1 if m.group(3) else 0}>"  # ncu's spelling
     if not any(want in k.get("kernel", "") for k in d.get("kernels", [])):
         return None, None
     return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")

@@ -44,9 +44,12 @@ struct Variant {
     {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>, 0, nullptr, nullptr, nullptr}
 // CTA-synchronised variants that also carry the NEXT-3 scrambled-output and the
 // epoch-major instantiations
-#define VS(name, vec, npt, wps)                                                                            \
-    {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1>, 0, prngk::batch_kernel<vec, npt, 0, 1, 1>, \
-     prngk::batch_kernel_epoch<vec, npt, 0>, prngk::batch_kernel_epoch<vec, npt, 1>}
+#define VS(name, vec, npt, wps) VSA(name, vec, npt, wps, false)
+// ... with the .aligned CTA barrier in uniform rounds (AL, prngk::cta_barrier)
+#define VSA(name, vec, npt, wps, al)                                                                 \
+    {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1, 0, al>, 0,                   \
+     prngk::batch_kernel<vec, npt, 0, 1, 1, al>, prngk::batch_kernel_epoch<vec, npt, 0, al>,       \
+     prngk::batch_kernel_epoch<vec, npt, 1, al>}
 #define VT(name, npt, stages, wps) \
     {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages, nullptr, nullptr, nullptr}
 // Measured on B200 at numrn = 2^24 x 1000 through a non-reused 64 GiB ring
@@ -83,8 +86,13 @@ const Variant kVariants[] = {
     // one 32-B store per thread per iteration, 4 numbers/thread, CTA barrier, 4 warps/SM:
     // the default until session 2 of round 1 (now "auto" below 2^21 work-items)
     VS("v4n4s1", 4, 4, 4),
+    // CTA barrier form (exp29): the .aligned bar.sync in uniform rounds, non-.aligned
+    // barrier.sync otherwise -- v4n8s1 2.3 % faster with it at the bench shape, v4n4s1
+    // 5 % slower; "auto" uses v4n8s1a
+    VSA("v4n8s1a", 4, 8, 4, true),   VSA("v4n4s1a", 4, 4, 4, true),
 };
 #undef VT
+#undef VSA
 #undef VS
 #undef V
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
@@ -194,9 +202,10 @@ static bool absorbs(const prng *h, int vid, uint64_t nslots, uint32_t iters) {
 // same CTA-synchronised 4-warps-per-SM structure as v4n4s1.
 static const char *const kWideNames[] = {"v4n8s1", "v4n16s1", "v2n32s1"};
 // "auto": one 32-B store per thread per iteration and a CTA barrier, 8 numbers per thread
-// (2 KiB per warp-iteration) from this many work-items per handle, 4 below.  Measured on
-// B200 (profiles/r1_sweeps.md, "Default"): v4n8s1 writes 7-9 % faster than v4n4s1 at
-// 2^21..2^24 on some boxes and ties on others; v4n4s1 is ahead at 2^18 and 2^20.
+// (2 KiB per warp-iteration, v4n8s1a: .aligned barrier in uniform rounds) from this many
+// work-items per handle, 4 below (v4n4s1).  Measured on B200 (profiles/r1_sweeps.md,
+// "Default"): v4n8s1 writes 7-9 % faster than v4n4s1 at 2^21..2^24 on some boxes and ties
+// on others; v4n4s1 is ahead at 2^18 and 2^20.
 constexpr uint64_t kAutoWideFrom = 1ull << 21;
 
 static int variant_id(const char *name) {
@@ -210,7 +219,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
                  bool first_is_state, cudaStream_t s, prng_err_t *err) {
     int vid = h->kernel;
     if (vid == 0) {  // "auto"
-        vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1" : "v4n4s1");
+        vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1a" : "v4n4s1");
         // Anti-absorption, first choice: the narrowest wider variant whose live set exceeds
         // 2x L2 (output identical; measured honest and as fast).  Not with a user grid.
         if (h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 && absorbs(h, vid, nslots, iters)) {

@@ -264,12 +264,26 @@ struct Unit {
 // Fewer drifting write streams -> fewer concurrently open DRAM pages.
 enum PieceMode { FULL = 0, PARTIAL = 1, IDLE = 2 };
 
+// The per-iteration CTA barrier (named barrier 1 over the CTA's active warps).  The
+// non-.aligned form: the warps of one CTA reach it from different instructions (full and
+// partial pieces, the peeled first trip, idle trips), which `bar.sync` (= barrier.sync
+// .aligned) does not allow -- compute-sanitizer synccheck flags it.
+// AL = true: the CTA's warps are known to run identical instruction sequences this round
+// (all full pieces, same trip count), which is what the .aligned `bar.sync` requires.
+template <bool AL = false>
+__device__ __forceinline__ void cta_barrier(uint32_t threads) {
+    if constexpr (AL)
+        asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
+    else
+        asm volatile("barrier.sync 1, %0;" ::"r"(threads) : "memory");
+}
+
 __device__ __forceinline__ void cluster_arrive() {
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
-template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0>
+template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0, bool AL = false>
 __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uint32_t bar_threads,
                                           uint32_t trace_round) {
     constexpr int NV = NPT / VEC;
@@ -330,7 +344,7 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
                             p[v * 32 * VEC + e] = emit<OUT>(x[v * VEC + e]);
             }
         }
-        if constexpr (SYNC == 1 || SYNC == 3) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+        if constexpr (SYNC == 1 || SYNC == 3) cta_barrier<AL>(bar_threads);
         if constexpr (SYNC == 3) {
             // drift diagnostic: CTA-leader timestamps every 64 iterations
             if ((t & 63) == 0 && bar_threads > 0 && a.trace && threadIdx.x == 0) {
@@ -340,7 +354,10 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
                 a.trace[((uint64_t)blockIdx.x * a.rounds + trace_round) * per_round + (t >> 6)] = ts;
             }
         }
-        if constexpr (SYNC == 2) cluster_arrive();
+        if constexpr (SYNC == 2) {
+            if constexpr (MODE == PARTIAL) __syncwarp();  // reconverge: the cluster barrier is .aligned
+            cluster_arrive();
+        }
         if (++slot == a.nslots) {  // warp-uniform
             slot = 0;
             p -= wrap;
@@ -409,7 +426,8 @@ __device__ __forceinline__ Unit make_unit(const BatchArgs &a, uint64_t unit, uin
     return u;
 }
 
-template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0>
+// AL: use the .aligned CTA barrier in rounds where the CTA is uniform (see cta_barrier).
+template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0, bool AL = false>
 __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
     constexpr uint64_t PIECE = 32ull * NPT;
@@ -438,10 +456,25 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
         // warps of this CTA holding a unit in round r: a prefix of the CTA's warps
         const uint32_t bar_threads = 32u * (uint32_t)(nunits - first < wpb ? nunits - first : wpb);
         const uint64_t piece = unit % a.npieces;
-        if ((piece + 1) * PIECE <= a.count)
-            run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT>(a, u, bar_threads, r);
-        else
-            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL, OUT>(a, u, bar_threads, r);
+        if ((piece + 1) * PIECE <= a.count) {
+            if constexpr (AL && (SYNC == 1 || SYNC == 3)) {
+                // uniform round: every active warp of the CTA has a full piece and the same
+                // trip count (only the last piece can be partial, only the last chunk short)
+                const uint64_t last = first + bar_threads / 32 - 1;
+                const uint64_t pf = first % a.npieces;
+                const bool has_partial = a.count % PIECE != 0 && pf + (last - first) >= a.npieces - 1;
+                const bool same_trips = a.nchunks <= 1 || first / a.npieces == last / a.npieces ||
+                                        last / a.npieces + 1 < a.nchunks;
+                if (!has_partial && same_trips)
+                    run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, true>(a, u, bar_threads, r);
+                else
+                    run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false>(a, u, bar_threads, r);
+            } else {
+                run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false>(a, u, bar_threads, r);
+            }
+        } else {
+            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL, OUT, false>(a, u, bar_threads, r);
+        }
     }
 }
 
@@ -476,7 +509,7 @@ __device__ __forceinline__ void load_vec_wk(const uint64_t *p, uint64_t *x) {
 }
 
 // One unit of the epoch kernel: a piece through iterations [t_begin, t_begin + t_count).
-template <int VEC, int NPT, int OUT, bool FULL>
+template <int VEC, int NPT, int OUT, bool FULL, bool AL = false>
 __device__ __forceinline__ void epoch_unit(const BatchArgs &a, uint64_t *x, uint64_t base, uint32_t slot,
                                            uint32_t t_count, bool emit_first, uint32_t bar_threads) {
     constexpr int NV = NPT / VEC;
@@ -498,7 +531,7 @@ __device__ __forceinline__ void epoch_unit(const BatchArgs &a, uint64_t *x, uint
                 for (int q = 0; q < VEC; ++q)
                     if (base + (uint64_t)v * 32 * VEC + q < a.count) p[v * 32 * VEC + q] = emit<OUT>(x[v * VEC + q]);
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+        cta_barrier<AL>(bar_threads);
         if (++slot == a.nslots) {  // warp-uniform
             slot = 0;
             p -= wrap;
@@ -518,7 +551,7 @@ __device__ __forceinline__ void epoch_unit(const BatchArgs &a, uint64_t *x, uint
     }
 }
 
-template <int VEC, int NPT, int OUT = 0>
+template <int VEC, int NPT, int OUT = 0, bool AL = false>
 __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
     static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
     constexpr int NV = NPT / VEC;
@@ -544,7 +577,7 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
         const uint32_t slot_begin = (uint32_t)(((uint64_t)a.slot0 + t_begin) % a.nslots);
         for (uint64_t r = 0; r < kw_cta; ++r) {
             if (r >= kw) {  // no piece for this warp in round r: idle through its barriers
-                for (uint32_t t = 0; t < t_count; ++t) asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+                for (uint32_t t = 0; t < t_count; ++t) cta_barrier(bar_threads);
                 continue;
             }
             const uint64_t piece = r * nwarps + warp;
@@ -553,7 +586,12 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
             if ((piece + 1) * PIECE <= a.count) {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) load_vec_wk<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
-                epoch_unit<VEC, NPT, OUT, true>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
+                // uniform round: all of the CTA's active warps hold a full piece in round r
+                const uint64_t last = r * nwarps + cta_warp0 + bar_threads / 32 - 1;
+                if (AL && last < a.npieces && (last + 1) * PIECE <= a.count)
+                    epoch_unit<VEC, NPT, OUT, true, AL>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
+                else
+                    epoch_unit<VEC, NPT, OUT, true, false>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
             } else {  // the ragged last piece

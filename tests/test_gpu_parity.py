@@ -10,7 +10,7 @@ import paper_1609_01257_b200 as P
 from workloads import RAGGED_N, SEED_PARITY, SPEC_GRID_I, SPEC_GRID_N, sample_points, shard_range
 
 # variants compiled with the NEXT-3 scrambled-output instantiation (prng_engine.cu VS(...))
-STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1", "v4n16s1", "v2n32s1")
+STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1", "v4n16s1", "v2n32s1", "v4n8s1a", "v4n4s1a")
 
 
 def _kid(name):
@@ -183,7 +183,7 @@ def test_autotune_then_parity():
     assert np.array_equal(out, oracle.stream(n, i, SEED_PARITY))
 
 
-@pytest.mark.parametrize("kv", range(32))
+@pytest.mark.parametrize("kv", range(40))
 def test_every_variant_device_only_wrapping_ring(kv):
     """Each kernel variant through the device-only ring path (grid-strided rounds, ring
     wrap-around inside one launch), vs the oracle at the ring slots and the state."""
@@ -551,9 +551,10 @@ def test_anti_absorption_rule(n, i, R, epoch_opt, expect, out_kind):
             assert int(st[x]) == oracle.sample(int(x), i - 1, SEED_PARITY)
 
 
-@pytest.mark.parametrize("n,name", [(1 << 24, "v4n8s1"), ((1 << 21) - 1, "v4n4s1"), (1 << 21, "v4n8s1")])
+@pytest.mark.parametrize("n,name", [(1 << 24, "v4n8s1a"), ((1 << 21) - 1, "v4n4s1"), (1 << 21, "v4n8s1a"),
+                                    ((1 << 21) + 300, "v4n8s1a")])
 def test_auto_kernel_at_bench_shape(n, name):
-    """"auto" (id 0): v4n8s1 from 2^21 work-items, v4n4s1 below.  At the bench shape
+    """"auto" (id 0): v4n8s1a from 2^21 work-items, v4n4s1 below.  At the bench shape
     (2^24 x 1000, default 64 GiB ring = 512 slots) the live set is 512 x 592 x 2 KiB =
     620 MB > 2 x L2, so v4n8s1 runs in natural order; the last iteration and the state vs
     the oracle (sampled gids)."""

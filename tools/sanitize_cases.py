@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel
-family (CTA-sync, free-running, cluster, TMA bulk-store, time-parallel jump-ahead, star
-output, zero-copy), checked against the oracle.  Run from the repo root on a GPU box:
+family (CTA-sync, free-running, cluster, TMA bulk-store, time-parallel jump-ahead, epoch
+order, the anti-absorption substitution, star output, zero-copy), checked against the
+oracle.  Run from the repo root on a GPU box:
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py
 """
 import os
@@ -14,22 +15,26 @@ import oracle  # noqa: E402
 import paper_1609_01257_b200 as P  # noqa: E402
 
 names = [P.prng_kernel_variant_name(i) for i in range(P.prng_kernel_variants())]
-cases = [  # (n, iters, variant, mode, output)
-    (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0),   # time-parallel chunks (iters >= 512)
-    (1003, 9, "v2n8s1", P.PRNG_MODE_OVERLAP1, 1),      # star output, ragged n
-    (4100, 7, "v4n8", P.PRNG_MODE_SERIAL, 0),
-    (4096, 5, "v2n8c2", P.PRNG_MODE_OVERLAP2, 0),      # cluster barrier
-    (5000, 6, "t2n8", P.PRNG_MODE_OVERLAP2, 0),        # TMA bulk stores
-    (4096, 6, "v2n4s1", P.PRNG_MODE_ZEROCOPY, 0),      # zero-copy
+cases = [  # (n, iters, variant, mode, output, device-ring slots, PRNG_OPT_EPOCH_ITERS)
+    (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 1000, 0),  # time-parallel chunks (iters >= 512)
+    (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 16, 0),    # wrapping ring: epoch order, E = 16
+    (1003, 9, "v2n8s1", P.PRNG_MODE_OVERLAP1, 1, 16, 0),      # star output, ragged n
+    (4100, 7, "v4n8", P.PRNG_MODE_SERIAL, 0, 16, 0),
+    (4096, 5, "v2n8c2", P.PRNG_MODE_OVERLAP2, 0, 16, 0),      # cluster barrier
+    (5000, 6, "t2n8", P.PRNG_MODE_OVERLAP2, 0, 16, 0),        # TMA bulk stores
+    (4096, 6, "v2n4s1", P.PRNG_MODE_ZEROCOPY, 0, 16, 0),      # zero-copy
+    (70001, 40, "auto", P.PRNG_MODE_OVERLAP2, 1, 16, 7),      # forced epochs, star, ragged
+    (1 << 20, 70, "auto", P.PRNG_MODE_OVERLAP2, 0, 64, 0),    # anti-absorption: v2n32s1
 ]
 bad = 0
-for n, it, v, mode, out in cases:
+for n, it, v, mode, out, slots, epoch in cases:
     h = P.prng_create(n, 3)
     P.prng_set_option(h, P.PRNG_OPT_KERNEL, names.index(v))
     P.prng_set_option(h, P.PRNG_OPT_OUTPUT, out)
     P.prng_set_option(h, P.PRNG_OPT_MODE, mode)
     P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 0 if it > 100 else 2)
-    P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, 16)
+    P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, slots)
+    P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, epoch)
     buf = np.zeros((it, n), np.uint64)
     P.prng_init(h)
     P.prng_generate(h, it, P.SINK_COPY, P.CopySink(buf.ctypes.data_as(P.P64), n, 0, it, 0))
@@ -38,7 +43,8 @@ for n, it, v, mode, out in cases:
     P.prng_init(h)
     P.prng_generate(h, it)  # device only through the ring
     ok = ok and np.array_equal(P.prng_read_state(h, n), oracle.stream(n, it, 3)[-1])
+    vid, e = P.prng_last_launch(h)
     P.prng_destroy(h)
-    print(n, it, v, mode, out, "ok" if ok else "MISMATCH", flush=True)
+    print(n, it, v, mode, out, slots, epoch, "ran", names[vid], "E", e, "ok" if ok else "MISMATCH", flush=True)
     bad += not ok
 sys.exit(1 if bad else 0)
