@@ -90,6 +90,9 @@ const Variant kVariants[] = {
     // barrier.sync otherwise -- v4n8s1 2.3 % faster with it at the bench shape, v4n4s1
     // 5 % slower; "auto" uses v4n8s1a
     VSA("v4n8s1a", 4, 8, 4, true),   VSA("v4n4s1a", 4, 4, 4, true),
+    // CTA barrier every 2 / 4 iterations (experiment, .aligned in uniform rounds)
+    {"v4n8s2a", 4, 8, 0, 5, 1, 4, prngk::batch_kernel<4, 8, 0, 5, 0, true>, 0, nullptr, nullptr, nullptr},
+    {"v4n8s4a", 4, 8, 0, 6, 1, 4, prngk::batch_kernel<4, 8, 0, 6, 0, true>, 0, nullptr, nullptr, nullptr},
 };
 #undef VT
 #undef VSA

@@ -259,6 +259,7 @@ struct Unit {
 //            iteration's stores are issued, wait just before the next iteration's stores,
 //            so the xorshift arithmetic overlaps the barrier.  Warps without a piece in
 //            the last round still take part in the barriers (IDLE mode).
+//   5, 6  as 1, but the barrier only every 2 / 4 iterations (experiment)
 //   3  as 1, plus a %globaltimer trace (diagnostic: measured CTA drift of ~180 iterations
 //            at numrn = 2^24, i.e. the grid writes ~180 ring slots at once).
 // Fewer drifting write streams -> fewer concurrently open DRAM pages.
@@ -345,6 +346,10 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
             }
         }
         if constexpr (SYNC == 1 || SYNC == 3) cta_barrier<AL>(bar_threads);
+        if constexpr (SYNC == 5 || SYNC == 6) {  // CTA barrier every 2 / 4 iterations
+            constexpr uint32_t BI = SYNC == 5 ? 2 : 4;
+            if ((t & (BI - 1)) == BI - 1) cta_barrier<AL>(bar_threads);
+        }
         if constexpr (SYNC == 3) {
             // drift diagnostic: CTA-leader timestamps every 64 iterations
             if ((t & 63) == 0 && bar_threads > 0 && a.trace && threadIdx.x == 0) {
@@ -457,7 +462,7 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
         const uint32_t bar_threads = 32u * (uint32_t)(nunits - first < wpb ? nunits - first : wpb);
         const uint64_t piece = unit % a.npieces;
         if ((piece + 1) * PIECE <= a.count) {
-            if constexpr (AL && (SYNC == 1 || SYNC == 3)) {
+            if constexpr (AL && (SYNC == 1 || SYNC == 3 || SYNC == 5 || SYNC == 6)) {
                 // uniform round: every active warp of the CTA has a full piece and the same
                 // trip count (only the last piece can be partial, only the last chunk short)
                 const uint64_t last = first + bar_threads / 32 - 1;
