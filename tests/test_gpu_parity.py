@@ -890,10 +890,16 @@ def test_argument_errors_on_a_live_handle():
     try:
         for opt, bad in [(P.PRNG_OPT_MODE, 9), (P.PRNG_OPT_KERNEL, 999), (P.PRNG_OPT_OUTPUT, 2),
                          (P.PRNG_OPT_RING_PAD, 3), (P.PRNG_OPT_HOST_MEM, 7), (P.PRNG_OPT_PROFILE, 5),
-                         (P.PRNG_OPT_CTA_WARPS, 9), (99, 0)]:
+                         (P.PRNG_OPT_CTA_WARPS, 9), (P.PRNG_OPT_CHUNK_ITERS, -1), (P.PRNG_OPT_PIECE_ORDER, 2),
+                         (P.PRNG_OPT_EPOCH_ITERS, -2), (99, 0)]:
             with pytest.raises(P.PrngError) as e:
                 P.prng_set_option(h, opt, bad)
             assert e.value.code == P.PRNG_EINVAL, (opt, bad)
+        for opt, good in [(P.PRNG_OPT_CHUNK_ITERS, 17), (P.PRNG_OPT_PIECE_ORDER, 1), (P.PRNG_OPT_EPOCH_ITERS, -1)]:
+            P.prng_set_option(h, opt, good)
+            assert P.prng_get_option(h, opt) == good
+            P.prng_set_option(h, opt, 0)
+        assert P.prng_last_launch(h) == (-1, 0)  # nothing launched yet
         P.prng_init(h)
         buf = torch.zeros(8 * 1024 + 8, dtype=torch.int64, device="cuda")
         for ptr, pitch in [(buf.data_ptr() + 8, 1000), (buf.data_ptr(), 1001), (buf.data_ptr(), 996)]:
