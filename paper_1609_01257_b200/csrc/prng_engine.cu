@@ -52,6 +52,9 @@ struct Variant {
      prngk::batch_kernel_epoch<vec, npt, 1, al>}
 #define VT(name, npt, stages, wps) \
     {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages, nullptr, nullptr, nullptr}
+// CTA-coherent TMA stores (one cp.async.bulk of the CTA's whole chunk per iteration)
+#define VTC(name, npt, stages) \
+    {name, 4, npt, 0, 1, 1, 4, prngk::batch_kernel_tmac<npt, stages>, stages, nullptr, nullptr, nullptr}
 // Measured on B200 at numrn = 2^24 x 1000 through a non-reused 64 GiB ring
 // (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 16-/32-B vectors reach
 // 6.6-6.8 TB/s (~90 % of the same-box cudaMemset fill rate; one 32-B store per thread is
@@ -93,7 +96,11 @@ const Variant kVariants[] = {
     // CTA barrier every 2 / 4 iterations (experiment, .aligned in uniform rounds)
     {"v4n8s2a", 4, 8, 0, 5, 1, 4, prngk::batch_kernel<4, 8, 0, 5, 0, true>, 0, nullptr, nullptr, nullptr},
     {"v4n8s4a", 4, 8, 0, 6, 1, 4, prngk::batch_kernel<4, 8, 0, 6, 0, true>, 0, nullptr, nullptr, nullptr},
+    // CTA-coherent TMA bulk stores: the v4n8s1a structure, one 8 KiB bulk copy per CTA per
+    // iteration from a ring of S = 3 / 4 shared-memory stages
+    VTC("c4n8s3", 8, 3), VTC("c4n8s4", 8, 4), VTC("c4n8s8", 8, 8), VTC("c4n8s16", 8, 16),
 };
+#undef VTC
 #undef VT
 #undef VSA
 #undef VS
@@ -465,8 +472,12 @@ prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begi
     if ((e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
         return bail("cudaDeviceGetAttribute(SMs)", e);
     cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, dev);
+    int smem_optin = 48 * 1024;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     for (int i = 0; i < kNumVariants; ++i) {
-        const size_t smem = variant_smem(kVariants[i], kBlock / 32);
+        // stage kernels size their shared memory per launch (warps per CTA x stages); allow
+        // up to the opt-in maximum, and size occupancy for the largest CTA that fits
+        const size_t smem = std::min<size_t>(variant_smem(kVariants[i], kBlock / 32), (size_t)smem_optin);
         if (smem > 48 * 1024 &&
             (e = cudaFuncSetAttribute(kVariants[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
                 cudaSuccess)

@@ -691,4 +691,88 @@ __global__ void __launch_bounds__(256) batch_kernel_tma(BatchArgs a) {
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+
+// ---------------------------------------------------------------- a2+a3: CTA-coherent TMA stores
+// The bench kernel's structure (4 warps per SM, adjacent pieces, CTA barrier every
+// iteration, VEC = 4) with the CTA's whole chunk for an iteration -- wpb x 32 x NPT x 8 B
+// contiguous (8 KiB for v4n8) -- written by ONE bulk async copy from shared memory instead
+// of 32-B STGs.  Per iteration t (stage t mod S):
+//   every lane STS its values into the stage at the chunk's layout, fence.proxy.async;
+//   thread 0 waits until at most S-2 bulk groups are pending reads (so the stage of
+//   iteration t+1 is free); CTA barrier; thread 0 issues cp.async.bulk + commit.
+// Rounds in which the CTA is not uniform (a partial piece, fewer active warps) take the
+// STG path (run_piece).  Natural order only (no chunks / epochs: the host never picks them
+// for stage kernels).
+template <int NPT, int S>
+__global__ void __launch_bounds__(256) batch_kernel_tmac(BatchArgs a) {
+    constexpr int VEC = 4, NV = NPT / VEC;
+    constexpr uint64_t PIECE = 32ull * NPT;
+    extern __shared__ __align__(128) uint64_t smem_tmac[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t wib = threadIdx.x >> 5;
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t cta_warp0 = (uint64_t)blockIdx.x * wpb;
+    const uint64_t chunk_elems = wpb * PIECE;
+    const uint32_t chunk_bytes = (uint32_t)(chunk_elems * sizeof(uint64_t));
+    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
+    for (uint32_t r = 0; r < a.rounds; ++r) {
+        const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
+        const uint64_t unit = first + wib;
+        if (unit >= a.npieces) break;  // warp-uniform
+        const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - first < wpb ? a.npieces - first : wpb);
+        const bool uniform = bar_threads == blockDim.x && (first + wpb) * PIECE <= a.count;
+        if (!uniform) {  // STG path (partial piece / fewer warps in the round)
+            const Unit u = make_unit<NPT, VEC>(a, unit, lane);
+            if ((unit + 1) * PIECE <= a.count)
+                run_piece<VEC, NPT, 0, 1, FULL, 0, false>(a, u, bar_threads, r);
+            else
+                run_piece<VEC, NPT, 0, 1, PARTIAL, 0, false>(a, u, bar_threads, r);
+            continue;
+        }
+        const uint64_t base = unit * PIECE + (uint64_t)lane * VEC;
+        uint64_t x[NPT];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+        uint32_t slot = a.slot0;
+        uint64_t *g = a.dst + (uint64_t)slot * a.pitch + first * PIECE;  // the CTA's chunk
+        for (uint32_t t = 0; t < a.iters; ++t) {
+            if (t > 0 || !a.first_is_state) {
+#pragma unroll
+                for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
+            }
+            uint64_t *sb = smem_tmac + (uint64_t)(t % S) * chunk_elems + (uint64_t)wib * PIECE;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sb + v * 32 * VEC + lane * VEC);
+                asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa), "l"(x[v * VEC]), "l"(x[v * VEC + 1]) : "memory");
+                asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa + 16), "l"(x[v * VEC + 2]), "l"(x[v * VEC + 3])
+                             : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - 2) : "memory");
+            cta_barrier<true>(bar_threads);
+            if (threadIdx.x == 0) {
+                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_tmac + (uint64_t)(t % S) * chunk_elems);
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa), "r"(chunk_bytes)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            if (++slot == a.nslots) {
+                slot = 0;
+                g -= wrap;
+            } else {
+                g += a.pitch;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+        // the next round (or the STG path) reuses the stages: drain the pending reads
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        cta_barrier<true>(bar_threads);
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 }  // namespace prngk
