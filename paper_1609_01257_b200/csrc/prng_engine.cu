@@ -53,8 +53,8 @@ struct Variant {
 #define VT(name, npt, stages, wps) \
     {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages, nullptr, nullptr, nullptr}
 // CTA-coherent TMA stores (one cp.async.bulk of the CTA's whole chunk per iteration)
-#define VTC(name, npt, stages) \
-    {name, 4, npt, 0, 1, 1, 4, prngk::batch_kernel_tmac<npt, stages>, stages, nullptr, nullptr, nullptr}
+#define VTC(name, npt, stages, pw) \
+    {name, 4, npt, 0, 1, 1, 4, prngk::batch_kernel_tmac<npt, stages, pw>, stages, nullptr, nullptr, nullptr}
 // Measured on B200 at numrn = 2^24 x 1000 through a non-reused 64 GiB ring
 // (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 16-/32-B vectors reach
 // 6.6-6.8 TB/s (~90 % of the same-box cudaMemset fill rate; one 32-B store per thread is
@@ -98,7 +98,10 @@ const Variant kVariants[] = {
     {"v4n8s4a", 4, 8, 0, 6, 1, 4, prngk::batch_kernel<4, 8, 0, 6, 0, true>, 0, nullptr, nullptr, nullptr},
     // CTA-coherent TMA bulk stores: the v4n8s1a structure, one 8 KiB bulk copy per CTA per
     // iteration from a ring of S = 3 / 4 shared-memory stages
-    VTC("c4n8s3", 8, 3), VTC("c4n8s4", 8, 4), VTC("c4n8s8", 8, 8), VTC("c4n8s16", 8, 16),
+    VTC("c4n8s3", 8, 3, false), VTC("c4n8s4", 8, 4, false), VTC("c4n8s8", 8, 8, false),
+    VTC("c4n8s16", 8, 16, false),
+    // ... one bulk copy per warp (its own 2 KiB piece) after the CTA barrier
+    VTC("w4n8s4", 8, 4, true), VTC("w4n8s8", 8, 8, true),
 };
 #undef VTC
 #undef VT

@@ -703,7 +703,9 @@ __global__ void __launch_bounds__(256) batch_kernel_tma(BatchArgs a) {
 // Rounds in which the CTA is not uniform (a partial piece, fewer active warps) take the
 // STG path (run_piece).  Natural order only (no chunks / epochs: the host never picks them
 // for stage kernels).
-template <int NPT, int S>
+// PW = true: each warp's lane 0 issues the bulk copy of the warp's own piece (wpb
+// streams per SM) instead of thread 0 issuing the CTA's chunk (one stream per SM).
+template <int NPT, int S, bool PW = false>
 __global__ void __launch_bounds__(256) batch_kernel_tmac(BatchArgs a) {
     constexpr int VEC = 4, NV = NPT / VEC;
     constexpr uint64_t PIECE = 32ull * NPT;
@@ -751,12 +753,19 @@ __global__ void __launch_bounds__(256) batch_kernel_tmac(BatchArgs a) {
                              : "memory");
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - 2) : "memory");
+            const bool issuer = PW ? lane == 0 : threadIdx.x == 0;
+            if (issuer) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - 2) : "memory");
             cta_barrier<true>(bar_threads);
-            if (threadIdx.x == 0) {
-                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_tmac + (uint64_t)(t % S) * chunk_elems);
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa), "r"(chunk_bytes)
-                             : "memory");
+            if (issuer) {
+                if constexpr (PW) {
+                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sb);
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g + wib * PIECE),
+                                 "r"(sa), "n"((uint32_t)(PIECE * 8)) : "memory");
+                } else {
+                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_tmac + (uint64_t)(t % S) * chunk_elems);
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa),
+                                 "r"(chunk_bytes) : "memory");
+                }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
             if (++slot == a.nslots) {
@@ -769,10 +778,10 @@ __global__ void __launch_bounds__(256) batch_kernel_tmac(BatchArgs a) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
         // the next round (or the STG path) reuses the stages: drain the pending reads
-        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (PW ? lane == 0 : threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         cta_barrier<true>(bar_threads);
     }
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (PW ? lane == 0 : threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace prngk
