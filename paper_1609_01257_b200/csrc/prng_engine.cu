@@ -98,6 +98,8 @@ const Variant kVariants[] = {
     {"v4n8s4a", 4, 8, 0, 6, 1, 4, prngk::batch_kernel<4, 8, 0, 6, 0, true>, 0, nullptr, nullptr, nullptr},
     // CTA-coherent TMA bulk stores: the v4n8s1a structure, one 8 KiB bulk copy per CTA per
     // iteration from a ring of S = 3 / 4 shared-memory stages
+    // v4n8s1a with the CTA's warps interleaving their vectors over the CTA's chunk
+    {"v4n8s1ai", 4, 8, 0, 1, 1, 4, prngk::batch_kernel<4, 8, 0, 1, 0, true, true>, 0, nullptr, nullptr, nullptr},
     VTC("c4n8s3", 8, 3, false), VTC("c4n8s4", 8, 4, false), VTC("c4n8s8", 8, 8, false),
     VTC("c4n8s16", 8, 16, false),
     // ... one bulk copy per warp (its own 2 KiB piece) after the CTA barrier

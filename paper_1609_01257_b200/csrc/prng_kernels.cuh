@@ -284,16 +284,21 @@ __device__ __forceinline__ void cluster_arrive() {
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
-template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0, bool AL = false>
+// IL (full pieces only): the lane's NPT / VEC vectors are `ilstride` elements apart instead
+// of 32 x VEC -- the CTA's warps interleave their vectors over the CTA's contiguous chunk
+// (u.base set accordingly by the caller), so each store instruction wave of the CTA covers
+// one contiguous wpb x 32 x VEC x 8 B run.
+template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0, bool AL = false, bool IL = false>
 __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uint32_t bar_threads,
-                                          uint32_t trace_round) {
+                                          uint32_t trace_round, uint64_t ilstride = 0) {
     constexpr int NV = NPT / VEC;
     const uint64_t base = u.base;
+    const uint64_t vs = IL ? ilstride : 32ull * VEC;  // elements between a lane's vectors
     uint64_t x[NPT];
     // ---- load the NPT states of this lane (read once per unit)
     if constexpr (MODE == FULL) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+        for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * vs, x + v * VEC);
     } else if constexpr (MODE == PARTIAL) {
 #pragma unroll
         for (int v = 0; v < NV; ++v)
@@ -328,12 +333,12 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     if constexpr (OUT == 0) {
-                        store_vec<VEC, POLICY>(p + v * 32 * VEC, x + v * VEC);
+                        store_vec<VEC, POLICY>(p + v * vs, x + v * VEC);
                     } else {
                         uint64_t y[VEC];
 #pragma unroll
                         for (int e = 0; e < VEC; ++e) y[e] = emit<OUT>(x[v * VEC + e]);
-                        store_vec<VEC, POLICY>(p + v * 32 * VEC, y);
+                        store_vec<VEC, POLICY>(p + v * vs, y);
                     }
                 }
             } else if constexpr (MODE == PARTIAL) {
@@ -394,7 +399,7 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
     if (u.state_out) {
         if constexpr (MODE == FULL) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(u.state_out + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+            for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(u.state_out + base + (uint64_t)v * vs, x + v * VEC);
         } else if constexpr (MODE == PARTIAL) {
 #pragma unroll
             for (int v = 0; v < NV; ++v)
@@ -432,7 +437,7 @@ __device__ __forceinline__ Unit make_unit(const BatchArgs &a, uint64_t unit, uin
 }
 
 // AL: use the .aligned CTA barrier in rounds where the CTA is uniform (see cta_barrier).
-template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0, bool AL = false>
+template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0, bool AL = false, bool IL = false>
 __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
     constexpr uint64_t PIECE = 32ull * NPT;
@@ -470,9 +475,21 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
                 const bool has_partial = a.count % PIECE != 0 && pf + (last - first) >= a.npieces - 1;
                 const bool same_trips = a.nchunks <= 1 || first / a.npieces == last / a.npieces ||
                                         last / a.npieces + 1 < a.nchunks;
-                if (!has_partial && same_trips)
+                if (!has_partial && same_trips) {
+                    if constexpr (IL) {
+                        // interleave the CTA's vectors over its chunk (contiguous pieces of
+                        // one iteration chunk: natural order, no chunk boundary inside)
+                        if (!a.order && first / a.npieces == last / a.npieces) {
+                            const uint64_t nact = bar_threads / 32;
+                            Unit ui = u;
+                            ui.base = pf * PIECE + ((warp - cta_warp0) * 32 + lane) * VEC;
+                            run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, true, true>(a, ui, bar_threads, r,
+                                                                                    nact * 32 * VEC);
+                            continue;
+                        }
+                    }
                     run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, true>(a, u, bar_threads, r);
-                else
+                } else
                     run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false>(a, u, bar_threads, r);
             } else {
                 run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false>(a, u, bar_threads, r);
