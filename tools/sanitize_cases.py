@@ -25,6 +25,10 @@ cases = [  # (n, iters, variant, mode, output, device-ring slots, PRNG_OPT_EPOCH
     (4096, 6, "v2n4s1", P.PRNG_MODE_ZEROCOPY, 0, 16, 0),      # zero-copy
     (70001, 40, "auto", P.PRNG_MODE_OVERLAP2, 1, 16, 7),      # forced epochs, star, ragged
     (1 << 20, 70, "auto", P.PRNG_MODE_OVERLAP2, 0, 64, 0),    # anti-absorption: v2n32s1
+    (300000, 9, "v4n8s1a", P.PRNG_MODE_OVERLAP2, 0, 16, 0),   # .aligned barrier in uniform rounds
+    (300000, 9, "v4n8s1ai", P.PRNG_MODE_OVERLAP2, 0, 16, 0),  # interleaved CTA vectors
+    (300000, 9, "c4n8s4", P.PRNG_MODE_OVERLAP2, 0, 16, 0),    # CTA-coherent TMA bulk stores
+    (300000, 9, "w4n8s4", P.PRNG_MODE_OVERLAP2, 0, 16, 0),    # per-warp TMA bulk stores + CTA barrier
 ]
 bad = 0
 for n, it, v, mode, out, slots, epoch in cases:
