@@ -1,7 +1,7 @@
 #!/bin/bash
 # Session-2 closing check on the committed tree: full GPU suite, smoke, bench (default),
 # reference arm, a sustained bench (200 steps, power-capped), launch list.
-OUT=gpurun_out/final_s2; mkdir -p $OUT
+OUT=gpurun_out/${1:-final_s2}; mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 timeout 1500 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
