@@ -295,6 +295,9 @@ int prng_prof_export(uint64_t nevents, const uint32_t *name_id, const double *st
 /* Same-box denominators: each returns GB/s (best of `reps`) or < 0 on
  * error.  bytes: buffer size. */
 double prng_probe_memset_gbs(uint64_t bytes, int reps);        /* cudaMemsetAsync write BW  */
+/* The same fill repeated `reps` times back to back, timed as one interval (sustained,
+ * power-capped write rate of the fill engine). */
+double prng_probe_memset_sustained_gbs(uint64_t bytes, int reps);
 double prng_probe_store_gbs(uint64_t bytes, int reps);         /* pure 32-B store kernel     */
 /* pattern 0 index, 1 zeros, 2 pseudo-random; warps_per_sm 0 = full occupancy */
 double prng_probe_store_pattern_gbs(uint64_t bytes, int reps, int pattern, int warps_per_sm);

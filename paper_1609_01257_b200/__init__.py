@@ -105,6 +105,7 @@ def lib():
         "prng_prof_summary": ([u64, vp, vp, vp, u32, vp, dbl, i32, i32, vp, u64, P64, E], i32),
         "prng_prof_export": ([u64, vp, vp, vp, u32, vp, vp, ctypes.c_char_p, E], i32),
         "prng_probe_memset_gbs": ([u64, i32], dbl),
+        "prng_probe_memset_sustained_gbs": ([u64, i32], dbl),
         "prng_probe_store_gbs": ([u64, i32], dbl),
         "prng_probe_store_pattern_gbs": ([u64, i32, i32, i32], dbl),
         "prng_probe_d2h_gbs": ([u64, i32, i32, i32], dbl),
@@ -368,6 +369,10 @@ def prng_prof_export(path: str, name_id, start_s, end_s, nnames: int = 4, names=
 
 def prng_probe_memset_gbs(nbytes: int, reps: int = 5) -> float:
     return lib().prng_probe_memset_gbs(nbytes, reps)
+
+
+def prng_probe_memset_sustained_gbs(nbytes: int, reps: int = 100) -> float:
+    return lib().prng_probe_memset_sustained_gbs(nbytes, reps)
 
 
 def prng_probe_store_gbs(nbytes: int, reps: int = 5) -> float:

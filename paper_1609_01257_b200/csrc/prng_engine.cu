@@ -45,6 +45,11 @@ struct Variant {
 // CTA-synchronised variants that also carry the NEXT-3 scrambled-output and the
 // epoch-major instantiations
 #define VS(name, vec, npt, wps) VSA(name, vec, npt, wps, false)
+// ... with the ping-pong hot loop (PP, prngk::run_piece)
+#define VSP(name, vec, npt, wps, al)                                                                      \
+    {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1, 0, al, false, true>, 0,             \
+     prngk::batch_kernel<vec, npt, 0, 1, 1, al, false, true>, prngk::batch_kernel_epoch<vec, npt, 0, al>, \
+     prngk::batch_kernel_epoch<vec, npt, 1, al>}
 // ... with the .aligned CTA barrier in uniform rounds (AL, prngk::cta_barrier)
 #define VSA(name, vec, npt, wps, al)                                                                 \
     {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1, 0, al>, 0,                   \
@@ -61,8 +66,8 @@ struct Variant {
 // ~2 % ahead of two 16-B ones, 7.29 TB/s at numrn = 2^27); free-running warps at full
 // occupancy ~6.2 TB/s (more concurrently open DRAM pages).
 const Variant kVariants[] = {
-    // id 0 "auto" (the default): resolved per launch by launch_batch -- v4n8s1 at >= 2^21
-    // work-items per handle, v4n4s1 below (measured), then widened or run in
+    // id 0 "auto" (the default): resolved per launch by launch_batch -- v4n8s1a at >= 2^21
+    // work-items per handle, v4n4s1p below (measured), then widened or run in
     // epoch order by the anti-absorption rule.  Its own fields (= v4n4s1) size the grid.
     VS("auto", 4, 4, 4),
     VS("v2n8s1", 2, 8, 4),  VS("v2n16s1", 2, 16, 4), VS("v4n8s1", 4, 8, 4),
@@ -98,6 +103,8 @@ const Variant kVariants[] = {
     {"v4n8s4a", 4, 8, 0, 6, 1, 4, prngk::batch_kernel<4, 8, 0, 6, 0, true>, 0, nullptr, nullptr, nullptr},
     // CTA-coherent TMA bulk stores: the v4n8s1a structure, one 8 KiB bulk copy per CTA per
     // iteration from a ring of S = 3 / 4 shared-memory stages
+    // ping-pong hot loop: no register copies before the 32-B stores
+    VSP("v4n8s1p", 4, 8, 4, true), VSP("v4n4s1p", 4, 4, 4, false),
     // v4n8s1a with the CTA's warps interleaving their vectors over the CTA's chunk
     {"v4n8s1ai", 4, 8, 0, 1, 1, 4, prngk::batch_kernel<4, 8, 0, 1, 0, true, true>, 0, nullptr, nullptr, nullptr},
     VTC("c4n8s3", 8, 3, false), VTC("c4n8s4", 8, 4, false), VTC("c4n8s8", 8, 8, false),
@@ -107,6 +114,7 @@ const Variant kVariants[] = {
 };
 #undef VTC
 #undef VT
+#undef VSP
 #undef VSA
 #undef VS
 #undef V
@@ -218,7 +226,8 @@ static bool absorbs(const prng *h, int vid, uint64_t nslots, uint32_t iters) {
 static const char *const kWideNames[] = {"v4n8s1", "v4n16s1", "v2n32s1"};
 // "auto": one 32-B store per thread per iteration and a CTA barrier, 8 numbers per thread
 // (2 KiB per warp-iteration, v4n8s1a: .aligned barrier in uniform rounds) from this many
-// work-items per handle, 4 below (v4n4s1).  Measured on B200 (profiles/r1_sweeps.md,
+// work-items per handle, 4 below (v4n4s1p: ping-pong hot loop, +2.5-3 % over v4n4s1 at the
+// bench shape, exp35).  Measured on B200 (profiles/r1_sweeps.md,
 // "Default"): v4n8s1 writes 7-9 % faster than v4n4s1 at 2^21..2^24 on some boxes and ties
 // on others; v4n4s1 is ahead at 2^18 and 2^20.
 constexpr uint64_t kAutoWideFrom = 1ull << 21;
@@ -234,7 +243,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
                  bool first_is_state, cudaStream_t s, prng_err_t *err) {
     int vid = h->kernel;
     if (vid == 0) {  // "auto"
-        vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1a" : "v4n4s1");
+        vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1a" : "v4n4s1p");
         // Anti-absorption, first choice: the narrowest wider variant whose live set exceeds
         // 2x L2 (output identical; measured honest and as fast).  Not with a user grid.
         if (h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 && absorbs(h, vid, nslots, iters)) {
@@ -811,8 +820,8 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
 static const struct {
     const char *variant;
     int warps_per_sm;
-} kTuneCandidates[] = {{"v4n4s1", 4}, {"v2n4s1", 4}, {"v2n4s1", 8}, {"v2n8s1", 4},
-                       {"v2n16s1", 4}, {"v2n8c2", 4}, {"v4n8s1", 4}, {"t2n8w8", 8}};
+} kTuneCandidates[] = {{"v4n4s1p", 4}, {"v2n4s1", 4}, {"v2n4s1", 8}, {"v2n8s1", 4},
+                       {"v2n16s1", 4}, {"v2n8c2", 4}, {"v4n8s1a", 4}, {"t2n8w8", 8}};
 
 extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err) {
     if (int rc = check_handle(h, err, false)) return rc;

@@ -288,7 +288,12 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 // of 32 x VEC -- the CTA's warps interleave their vectors over the CTA's contiguous chunk
 // (u.base set accordingly by the caller), so each store instruction wave of the CTA covers
 // one contiguous wpb x 32 x VEC x 8 B run.
-template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0, bool AL = false, bool IL = false>
+// PP: the hot loop is unrolled by two with the state ping-ponging between two register
+// arrays, so each step's results land directly in the registers the next 32-B store
+// reads (without it ptxas copies 8 registers into a staging octet before every STG.256:
+// 16 extra IMAD.MOV per iteration at NPT = 8, 13 % of the loop's instructions).
+template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0, bool AL = false, bool IL = false,
+          bool PP = false>
 __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uint32_t bar_threads,
                                           uint32_t trace_round, uint64_t ilstride = 0) {
     constexpr int NV = NPT / VEC;
@@ -324,7 +329,7 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
     // barrier, advance to the next ring slot.  Every unit of a launch makes the same number
     // of trips (the barriers of SYNC 1 / 2 must match): a shorter last chunk idles through
     // its surplus trips.  The first trip is peeled so the hot loop has no conditions.
-    auto trip = [&](uint32_t t, bool active) {
+    auto trip = [&](uint32_t t, bool active, const uint64_t *src) {
         if constexpr (SYNC == 2) {
             if (t > 0) cluster_wait();
         }
@@ -333,11 +338,11 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     if constexpr (OUT == 0) {
-                        store_vec<VEC, POLICY>(p + v * vs, x + v * VEC);
+                        store_vec<VEC, POLICY>(p + v * vs, src + v * VEC);
                     } else {
                         uint64_t y[VEC];
 #pragma unroll
-                        for (int e = 0; e < VEC; ++e) y[e] = emit<OUT>(x[v * VEC + e]);
+                        for (int e = 0; e < VEC; ++e) y[e] = emit<OUT>(src[v * VEC + e]);
                         store_vec<VEC, POLICY>(p + v * vs, y);
                     }
                 }
@@ -347,7 +352,7 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
 #pragma unroll
                     for (int e = 0; e < VEC; ++e)
                         if (base + (uint64_t)v * 32 * VEC + e < a.count)
-                            p[v * 32 * VEC + e] = emit<OUT>(x[v * VEC + e]);
+                            p[v * 32 * VEC + e] = emit<OUT>(src[v * VEC + e]);
             }
         }
         if constexpr (SYNC == 1 || SYNC == 3) cta_barrier<AL>(bar_threads);
@@ -386,14 +391,25 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
     uint32_t t = 0;
     if (t_act > 0) {
         if (!u.emit_first) step();
-        trip(0, true);
+        trip(0, true, x);
         t = 1;
     }
-    for (; t < t_act; ++t) {  // the hot loop
-        step();
-        trip(t, true);
+    if constexpr (PP && MODE == FULL) {
+        uint64_t y[NPT];
+        for (; t + 1 < t_act; t += 2) {  // the hot loop, two iterations per trip
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) y[j] = xorshift64(x[j]);
+            trip(t, true, y);
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(y[j]);
+            trip(t + 1, true, x);
+        }
     }
-    for (; t < t_loop; ++t) trip(t, false);  // idle trips (short last chunk, IDLE units)
+    for (; t < t_act; ++t) {  // the hot loop (PP: the odd last iteration)
+        step();
+        trip(t, true, x);
+    }
+    for (; t < t_loop; ++t) trip(t, false, x);  // idle trips (short last chunk, IDLE units)
     if constexpr (SYNC == 2) cluster_wait();  // balance the last arrive
     // ---- write the state back (== the unit's last iteration) if this unit ends the launch
     if (u.state_out) {
@@ -437,7 +453,7 @@ __device__ __forceinline__ Unit make_unit(const BatchArgs &a, uint64_t unit, uin
 }
 
 // AL: use the .aligned CTA barrier in rounds where the CTA is uniform (see cta_barrier).
-template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0, bool AL = false, bool IL = false>
+template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0, bool AL = false, bool IL = false, bool PP = false>
 __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
     constexpr uint64_t PIECE = 32ull * NPT;
@@ -488,11 +504,11 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
                             continue;
                         }
                     }
-                    run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, true>(a, u, bar_threads, r);
+                    run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, true, false, PP>(a, u, bar_threads, r);
                 } else
-                    run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false>(a, u, bar_threads, r);
+                    run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false, false, PP>(a, u, bar_threads, r);
             } else {
-                run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false>(a, u, bar_threads, r);
+                run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false, false, PP>(a, u, bar_threads, r);
             }
         } else {
             run_piece<VEC, NPT, POLICY, SYNC, PARTIAL, OUT, false>(a, u, bar_threads, r);

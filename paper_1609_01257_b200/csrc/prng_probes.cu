@@ -120,6 +120,25 @@ double prng_probe_memset_gbs(uint64_t bytes, int reps) {
     return cudaGetLastError() == cudaSuccess ? best : -1;
 }
 
+double prng_probe_memset_sustained_gbs(uint64_t bytes, int reps) {
+    void *p = nullptr;
+    if (reps < 1 || cudaMalloc(&p, bytes) != cudaSuccess) return -1;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaMemset(p, 1, bytes);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) cudaMemsetAsync(p, r & 0xff, bytes);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(p);
+    return cudaGetLastError() == cudaSuccess ? (double)bytes * reps / (ms * 1e-3) / 1e9 : -1;
+}
+
 double prng_probe_store_gbs(uint64_t bytes, int reps) { return prng_probe_store_pattern_gbs(bytes, reps, 0, 0); }
 
 double prng_probe_store_pattern_gbs(uint64_t bytes, int reps, int pattern, int warps_per_sm) {

@@ -10,7 +10,8 @@ import paper_1609_01257_b200 as P
 from workloads import RAGGED_N, SEED_PARITY, SPEC_GRID_I, SPEC_GRID_N, sample_points, shard_range
 
 # variants compiled with the NEXT-3 scrambled-output instantiation (prng_engine.cu VS(...))
-STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1", "v4n16s1", "v2n32s1", "v4n8s1a", "v4n4s1a")
+STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1", "v4n16s1", "v2n32s1", "v4n8s1a", "v4n4s1a",
+              "v4n8s1p", "v4n4s1p")
 
 
 def _kid(name):
@@ -494,10 +495,10 @@ def test_epoch_order(kname, epoch, out_kind):
 # (numrn, iterations, ring slots, epoch option, expected (variant, epoch length)); L2 = 126 MB
 # on B200, 592 warps: live set = R x min(592, pieces) x bytes per warp-iteration vs 2 x L2.
 ANTI_ABSORPTION = [
-    (300007, 1000, 16, 0, ("v4n4s1", 16)),   # no wide variant clears 2 x L2 and the widest has < 1 piece
+    (300007, 1000, 16, 0, ("v4n4s1p", 16)),  # no wide variant clears 2 x L2 and the widest has < 1 piece
                                              # per warp: epoch order on the default, E = R
-    (300007, 1000, 16, -1, ("v4n4s1", 0)),   # -1: natural order (absorbing) on request
-    (300007, 40, 64, 0, ("v4n4s1", 0)),      # no wrap inside the launch: nothing to absorb
+    (300007, 1000, 16, -1, ("v4n4s1p", 0)),  # -1: natural order (absorbing) on request
+    (300007, 40, 64, 0, ("v4n4s1p", 0)),     # no wrap inside the launch: nothing to absorb
     (1 << 20, 80, 64, 0, ("v2n32s1", 0)),    # 64 x 592 x 8 KiB = 310 MB: the 8 KiB variant
     (1 << 20, 310, 300, 0, ("v4n8s1", 0)),   # 300 x 592 x 2 KiB = 364 MB: the 2 KiB variant
     ((1 << 20) + 77, 80, 64, 0, ("v2n32s1", 0)),  # ragged
@@ -551,10 +552,10 @@ def test_anti_absorption_rule(n, i, R, epoch_opt, expect, out_kind):
             assert int(st[x]) == oracle.sample(int(x), i - 1, SEED_PARITY)
 
 
-@pytest.mark.parametrize("n,name", [(1 << 24, "v4n8s1a"), ((1 << 21) - 1, "v4n4s1"), (1 << 21, "v4n8s1a"),
+@pytest.mark.parametrize("n,name", [(1 << 24, "v4n8s1a"), ((1 << 21) - 1, "v4n4s1p"), (1 << 21, "v4n8s1a"),
                                     ((1 << 21) + 300, "v4n8s1a")])
 def test_auto_kernel_at_bench_shape(n, name):
-    """"auto" (id 0): v4n8s1a from 2^21 work-items, v4n4s1 below.  At the bench shape
+    """"auto" (id 0): v4n8s1a from 2^21 work-items, v4n4s1p below.  At the bench shape
     (2^24 x 1000, default 64 GiB ring = 512 slots) the live set is 512 x 592 x 2 KiB =
     620 MB > 2 x L2, so v4n8s1 runs in natural order; the last iteration and the state vs
     the oracle (sampled gids)."""

@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 import paper_1609_01257_b200 as P  # noqa: E402
 
-names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["v2n4s1", "v4n8s1", "v4n12s1", "v4n16s1"]
+names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["v4n8s1a", "v4n4s1"]
 rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 torch.cuda.set_device(0)
@@ -23,7 +23,10 @@ for nm in names:
     h = P.prng_create(n, 0)
     P.prng_set_streams(h, gen.cuda_stream, cop.cuda_stream)
     P.prng_set_option(h, P.PRNG_OPT_KERNEL, allv.index(nm))
-    P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, 128)  # 16 GiB each (4 handles share the GPU)
+    # 512 slots = 64 GiB per handle: the live set (512 x 592 warps x >= 1 KiB) clears 2 x L2,
+    # so no rewrite is absorbed in L2 (profiles/r1_l2_absorption.md; round 1 used 128 slots,
+    # 16 GiB, whose rewrites were partly absorbed).  Two handles fit in HBM.
+    P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, 512)
     P.prng_init(h)
     P.prng_generate(h, it)
     hs[nm] = h
@@ -43,3 +46,8 @@ for r in range(rounds):
 for nm in names:
     print(json.dumps({"variant": nm, "median_gbs": round(statistics.median(res[nm]), 1),
                       "min": round(min(res[nm]), 1), "max": round(max(res[nm]), 1)}))
+for h in hs.values():
+    P.prng_destroy(h)
+# the fill engine sustained over a comparable time (~4 s of 32 GiB fills), for reference
+print(json.dumps({"variant": "cudaMemsetAsync (sustained)",
+                  "gbs": round(P.prng_probe_memset_sustained_gbs(32 << 30, 900), 1)}))
