@@ -153,9 +153,10 @@ enum prng_option {
                                   prng_init; 2 = same, accumulated across prng_init calls
                                   and without the host syncs mode 1 adds for wall time    */
     PRNG_OPT_KERNEL = 5,       /* kernel variant id (see prng_kernel_variants); 0 = "auto"
-                                  (default): v4n8s1 from 2^21 work-items per handle, v4n4s1
-                                  below, widened / epoch-ordered by the anti-absorption rule
-                                  (see PRNG_OPT_EPOCH_ITERS, prng_last_launch)            */
+                                  (default): v4n8s1a from 2^21 work-items per handle,
+                                  v4n4s1p below, widened / epoch-ordered by the
+                                  anti-absorption rule (see PRNG_OPT_EPOCH_ITERS,
+                                  prng_last_launch)                                       */
     PRNG_OPT_GRID_WARPS = 6,   /* cap on resident warps of the persistent grid; 0 = auto  */
     PRNG_OPT_RING_PAD = 7,     /* extra u64 elements between device-only ring slots (multiple
                                   of 4; breaks power-of-two slot strides); default 0       */
@@ -166,9 +167,9 @@ enum prng_option {
     PRNG_OPT_OUTPUT = 10,      /* NEXT-3 output transform: 0 = the state (the paper, A7);
                                   1 = state * 0x2545F4914F6CDD1D mod 2^64 (xorshift64*-style
                                   scrambler, A19).  Needs a CTA-synchronised variant with
-                                  a scrambled instantiation (v4n4s1, v2n8s1, v2n16s1,
-                                  v4n8s1, v2n4s1, v4n16s1, v2n32s1); others give
-                                  PRNG_EINVAL.                                         */
+                                  a scrambled instantiation ("auto", v4n4s1, v2n8s1,
+                                  v2n16s1, v4n8s1, v2n4s1, v4n16s1, v2n32s1, v4n8s1a,
+                                  v4n4s1a, v4n8s1p, v4n4s1p); others give PRNG_EINVAL.   */
     PRNG_OPT_TIME_PARALLEL = 11, /* 1 (default): when numrn is too small to fill the GPU, cut
                                   a launch's iterations into chunks started by GF(2)
                                   jump-ahead (xs^k is linear: a 64x64 bit matrix); 0: off */
