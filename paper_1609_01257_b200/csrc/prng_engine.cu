@@ -105,6 +105,7 @@ const Variant kVariants[] = {
     // iteration from a ring of S = 3 / 4 shared-memory stages
     // ping-pong hot loop: no register copies before the 32-B stores
     VSP("v4n8s1p", 4, 8, 4, true), VSP("v4n4s1p", 4, 4, 4, false),
+    VSP("v4n16s1p", 4, 16, 4, true), VSP("v2n32s1p", 2, 32, 4, true),
     // v4n8s1a with the CTA's warps interleaving their vectors over the CTA's chunk
     {"v4n8s1ai", 4, 8, 0, 1, 1, 4, prngk::batch_kernel<4, 8, 0, 1, 0, true, true>, 0, nullptr, nullptr, nullptr},
     VTC("c4n8s3", 8, 3, false), VTC("c4n8s4", 8, 4, false), VTC("c4n8s8", 8, 8, false),
