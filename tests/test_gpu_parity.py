@@ -732,6 +732,41 @@ def test_bench_config_every_ring_slot():
         assert got_x[k] == int(wx[k]) and got_s[k] == int(ws[k]), k
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("lg,name", [(25, "v4n8s1a"), (26, "v4n16s1"), (27, "v2n32s1")])
+def test_config4_rank_shapes_every_ring_slot(lg, name):
+    """BASELINE config 4 at its per-rank shapes (2^28 over 8 / 4 / 2 GPUs = 2^25 / 2^26 /
+    2^27 per rank, 1000 iterations, default 64 GiB ring of 256 / 128 / 64 slots): the
+    kernel the anti-absorption rule runs, and for each iteration still in the ring the XOR
+    and wrapping sum of all its outputs (folded on the GPU) vs the oracle's digests."""
+    import torch
+    n, i = 1 << lg, 1000
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        assert (P.prng_kernel_variant_name(P.prng_last_launch(h)[0]), P.prng_last_launch(h)[1]) == (name, 0)
+        base, pitch, slots, first, end = P.prng_device_ring(h)
+        ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
+        got = {}
+        for k in range(i - slots, i):
+            row = ring[(first + k) % slots, :n]
+            s_ = int(row.sum().item()) & ((1 << 64) - 1)
+            v = row.clone()
+            m = v.numel()
+            while m > 1:
+                h2 = m // 2
+                v[:h2] ^= v[m - h2:m]
+                m -= h2
+            got[k] = (int(v[0].item()) & ((1 << 64) - 1), s_)
+            del v
+    finally:
+        P.prng_destroy(h)
+    wx, ws = _oracle_digest_threads(n, i, SEED_PARITY)
+    for k in range(i - slots, i):
+        assert got[k] == (int(wx[k]), int(ws[k])), k
+
+
 # ---------------------------------------------------------------- shared host output (north_star e)
 def test_generate_host_shards_fill_one_array():
     """Each 'rank' (one handle per gid shard) writes its columns of one host array directly."""
