@@ -234,9 +234,10 @@ def test_full_size_config2_sampled():
 
 @pytest.mark.slow
 def test_full_width_e2e_digests():
-    """Config 3's width (n = 2^24) end to end with per-iteration XOR / sum digests over every
-    output (numiter cut to 24 so the single-threaded oracle finishes in seconds)."""
-    n, i = 1 << 24, 24
+    """BASELINE config 3 in full (n = 2^24, 1000 iterations, end to end through the default
+    O2 pipeline: 134 GB over the host link) with per-iteration XOR / sum digests over every
+    output vs the oracle's digests (threaded over gid shards)."""
+    n, i = 1 << 24, 1000
     xo = np.zeros(i, np.uint64)
     so = np.zeros(i, np.uint64)
     d = P.DigestSink(xo.ctypes.data_as(P.P64), so.ctypes.data_as(P.P64), 0, i)
@@ -246,48 +247,7 @@ def test_full_width_e2e_digests():
         P.prng_generate(h, i, P.SINK_DIGEST, d)
     finally:
         P.prng_destroy(h)
-    wx, ws = oracle.digest(n, i, SEED_PARITY)
-    assert np.array_equal(xo, wx) and np.array_equal(so, ws)
-
-
-@pytest.mark.slow
-@pytest.mark.parametrize("mode", [P.PRNG_MODE_OVERLAP2, P.PRNG_MODE_ZEROCOPY])
-def test_config5_rank_shape_e2e_digests(mode):
-    """BASELINE config 5 at its per-rank shape (2^28 over 8 GPUs = 2^25 per rank, 100
-    iterations, end to end): a rank's gid range of the 2^28 stream (rank 3 of 8), through
-    the pinned double buffer (O2) and zero-copy (O3), with per-iteration XOR / sum digests
-    of every output vs the oracle's digests of the same gid range (threaded)."""
-    total, P8, r = 1 << 28, 8, 3
-    b, c = shard_range(total, r, P8)
-    i = 100
-    xo = np.zeros(i, np.uint64)
-    so = np.zeros(i, np.uint64)
-    d = P.DigestSink(xo.ctypes.data_as(P.P64), so.ctypes.data_as(P.P64), 0, i)
-    h = P.prng_create_range(total, SEED_PARITY, b, c)
-    try:
-        P.prng_set_option(h, P.PRNG_OPT_MODE, mode)
-        P.prng_init(h)
-        P.prng_generate(h, i, P.SINK_DIGEST, d)
-    finally:
-        P.prng_destroy(h)
-    import os
-    import threading
-    nth = max(1, len(os.sched_getaffinity(0)))
-    parts = [None] * nth
-
-    def work(t):
-        bb, cc = shard_range(c, t, nth)
-        parts[t] = oracle.digest(total, i, SEED_PARITY, gid_begin=b + bb, count=cc) if cc else None
-
-    th = [threading.Thread(target=work, args=(t,)) for t in range(nth)]
-    [x.start() for x in th]
-    [x.join() for x in th]
-    wx = np.zeros(i, np.uint64)
-    ws = np.zeros(i, np.uint64)
-    for p_ in parts:
-        if p_ is not None:
-            wx ^= p_[0]
-            ws += p_[1]
+    wx, ws = _oracle_digest_threads(n, i, SEED_PARITY)
     assert np.array_equal(xo, wx) and np.array_equal(so, ws)
 
 
