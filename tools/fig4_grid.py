@@ -40,6 +40,8 @@ def main():
         h = P.prng_create(n, 0)
         P.prng_set_streams(h, gen.cuda_stream, cop.cuda_stream)
         P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, ring)
+        if ring:  # the labelled L2-resident diagnostic: keep the natural order (no
+            P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, -1)  # anti-absorption rule)
         for it in (100, 1000, 10000):
             nbytes = 8 * n * it
             P.prng_init(h)
@@ -56,7 +58,9 @@ def main():
                 best = min(best or 1e30, e0.elapsed_time(e1))
             key = "device" if ring == 0 else "device_ring256"
             rows.setdefault((lg, it), {"n": f"2^{lg}", "i": it, "bytes": nbytes})
-            rows[(lg, it)].update({f"{key}_ms": best, f"{key}_gbs": nbytes / (best * 1e-3) / 1e9})
+            vid, ep = P.prng_last_launch(h)
+            rows[(lg, it)].update({f"{key}_ms": best, f"{key}_gbs": nbytes / (best * 1e-3) / 1e9,
+                                   f"{key}_kernel": P.prng_kernel_variant_name(vid) + (f"/E{ep}" if ep else "")})
         P.prng_destroy(h)
     # pass 2: end to end (host wall clock, null sink), bounded total bytes
     for lg in range(12, 25, 2):
