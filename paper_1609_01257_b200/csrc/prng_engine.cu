@@ -197,11 +197,14 @@ int prof_end(prng *h, cudaStream_t s, prng_err_t *err) {
 }
 
 // Persistent grid of a variant: at most one wave of resident warps.
-static uint64_t max_grid_warps(const prng *h, int vid) {
+// wps > 0: warps per SM chosen by the anti-absorption rule instead of the variant's.
+static uint64_t max_grid_warps(const prng *h, int vid, int wps = 0) {
     const Variant &v = kVariants[vid];
     uint64_t w = (uint64_t)h->blocks_per_sm[vid] * h->num_sms * (kBlock / 32);
     if (h->grid_warps > 0)
         w = std::min<uint64_t>(w, (uint64_t)h->grid_warps);
+    else if (wps > 0)
+        w = std::min<uint64_t>(w, (uint64_t)wps * h->num_sms);
     else if (v.warps_per_sm > 0)
         w = std::min<uint64_t>(w, (uint64_t)v.warps_per_sm * h->num_sms);
     return std::max<uint64_t>(w, kBlock / 32);
@@ -214,13 +217,13 @@ static uint64_t max_grid_warps(const prng *h, int vid) {
 // hit dirty L2 lines and never reach DRAM (ncu: 12 % of the stores reach DRAM at
 // numrn = 2^27 through 64 slots).  That is not sustained output bandwidth, so such launches
 // are reorganised: a variant with more numbers per warp-iteration, or epoch order.
-static uint64_t live_bytes(const prng *h, int vid, uint64_t nslots) {
+static uint64_t live_bytes(const prng *h, int vid, uint64_t nslots, int wps = 0) {
     const uint64_t piece = 32ull * kVariants[vid].npt;
     const uint64_t npieces = (h->count + piece - 1) / piece;
-    return nslots * std::min<uint64_t>(max_grid_warps(h, vid), npieces) * piece * sizeof(uint64_t);
+    return nslots * std::min<uint64_t>(max_grid_warps(h, vid, wps), npieces) * piece * sizeof(uint64_t);
 }
-static bool absorbs(const prng *h, int vid, uint64_t nslots, uint32_t iters) {
-    return iters > nslots && live_bytes(h, vid, nslots) < 2 * (uint64_t)h->l2_bytes;
+static bool absorbs(const prng *h, int vid, uint64_t nslots, uint32_t iters, int wps = 0) {
+    return iters > nslots && live_bytes(h, vid, nslots, wps) < 2 * (uint64_t)h->l2_bytes;
 }
 // Default-variant substitutes in order of numbers per warp-iteration (2, 4, 8 KiB):
 // same CTA-synchronised 4-warps-per-SM structure as v4n4s1.
@@ -243,6 +246,7 @@ static int variant_id(const char *name) {
 int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64_t slot0, uint32_t iters,
                  bool first_is_state, cudaStream_t s, prng_err_t *err) {
     int vid = h->kernel;
+    int wps = 0;  // warps per SM override (anti-absorption, second choice)
     if (vid == 0) {  // "auto"
         vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1a" : "v4n4s1p");
         // Anti-absorption, first choice: the narrowest wider variant whose live set exceeds
@@ -259,6 +263,14 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
                     found = true;
                     break;
                 }
+            }
+            // second choice: the widest variant with twice the warps per SM (8), which
+            // doubles the live set (numrn = 2^28 through 32 slots: 6.2 TB/s, ncu DRAM
+            // bytes 99.6 % of the stores, vs 5.6 in epoch order; exp39)
+            if (!found && !absorbs(h, widest, nslots, iters, 2 * kVariants[widest].warps_per_sm)) {
+                vid = widest;
+                wps = 2 * kVariants[widest].warps_per_sm;
+                found = true;
             }
             // none clears 2x L2: epoch order below, on the widest variant (fewest units,
             // so the per-unit state round trip is amortised over the most stores) if it
@@ -294,7 +306,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     const uint64_t piece = 32ull * v.npt;
     a.npieces = (h->count + piece - 1) / piece;
     // Persistent grid: at most one wave of resident warps; equalise pieces per warp.
-    const uint64_t max_warps = max_grid_warps(h, vid);
+    const uint64_t max_warps = max_grid_warps(h, vid, wps);
     // Time-parallel mode (NEXT-4): when the pieces cannot fill the grid (small numrn), cut
     // the launch's iterations into chunks started by GF(2) jump-ahead, so that
     // pieces x chunks units fill it.
@@ -316,7 +328,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     if (v.epoch && nch <= 1 && h->epoch_iters >= 0) {
         if (h->epoch_iters > 0)
             E = (uint64_t)h->epoch_iters;  // PRNG_OPT_EPOCH_ITERS: forced
-        else if (absorbs(h, vid, nslots, iters))
+        else if (absorbs(h, vid, nslots, iters, wps))
             E = nslots;
         if (E >= iters) E = 0;
     }

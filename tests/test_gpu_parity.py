@@ -504,6 +504,7 @@ ANTI_ABSORPTION = [
     (1 << 20, 310, 300, 0, ("v4n8s1", 0)),   # 300 x 592 x 2 KiB = 364 MB: the 2 KiB variant
     ((1 << 20) + 77, 80, 64, 0, ("v2n32s1", 0)),  # ragged
     (1 << 20, 50, 8, 0, ("v2n32s1", 8)),     # none clears 2 x L2: epoch order on the widest, E = R
+    (1 << 21, 100, 40, 0, ("v2n32s1", 0)),   # widest at 8 warps/SM: 40 x 1184 x 8 KiB = 388 MB
 ]
 
 
