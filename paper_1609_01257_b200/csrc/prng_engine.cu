@@ -39,6 +39,8 @@ struct Variant {
     int stages;                           // > 0: TMA bulk-store kernel with this many smem stages
     BatchFn star;                         // NEXT-3 xorshift64* output instantiation (nullptr: none)
     BatchFn epoch, epoch_star;            // epoch-major instantiations (nullptr: none)
+    BatchFn lean = nullptr, lean_star = nullptr;  // single-path form for launches whose pieces
+                                                  // are all full, natural order (nullptr: none)
 };
 #define V(name, vec, npt, pol, sync, cl, wps) \
     {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>, 0, nullptr, nullptr, nullptr}
@@ -105,6 +107,13 @@ const Variant kVariants[] = {
     // iteration from a ring of S = 3 / 4 shared-memory stages
     // ping-pong hot loop: no register copies before the 32-B stores
     VSP("v4n8s1p", 4, 8, 4, true), VSP("v4n4s1p", 4, 4, 4, false),
+    // the same with the lean single-path kernel when every piece is full (batch_kernel_lean)
+    {"v4n8s1l", 4, 8, 0, 1, 1, 4, prngk::batch_kernel<4, 8, 0, 1, 0, true, false, true>, 0,
+     prngk::batch_kernel<4, 8, 0, 1, 1, true, false, true>, prngk::batch_kernel_epoch<4, 8, 0, true>,
+     prngk::batch_kernel_epoch<4, 8, 1, true>, prngk::batch_kernel_lean<4, 8, 0>, prngk::batch_kernel_lean<4, 8, 1>},
+    {"v4n4s1l", 4, 4, 0, 1, 1, 4, prngk::batch_kernel<4, 4, 0, 1, 0, false, false, true>, 0,
+     prngk::batch_kernel<4, 4, 0, 1, 1, false, false, true>, prngk::batch_kernel_epoch<4, 4, 0, false>,
+     prngk::batch_kernel_epoch<4, 4, 1, false>, prngk::batch_kernel_lean<4, 4, 0>, prngk::batch_kernel_lean<4, 4, 1>},
     VSP("v4n16s1p", 4, 16, 4, true), VSP("v2n32s1p", 2, 32, 4, true),
     // v4n8s1a with the CTA's warps interleaving their vectors over the CTA's chunk
     {"v4n8s1ai", 4, 8, 0, 1, 1, 4, prngk::batch_kernel<4, 8, 0, 1, 0, true, true>, 0, nullptr, nullptr, nullptr},
@@ -332,6 +341,10 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
             E = nslots;
         if (E >= iters) E = 0;
     }
+    // lean single-path kernel: every piece full, natural order, no chunks, default grid
+    // shape (one CTA of <= 8 warps per SM or 256-thread CTAs, as for the regular kernel)
+    if (v0.lean && E == 0 && nch <= 1 && a.order == 0 && h->count % piece == 0)
+        v.fn = h->output == 1 ? v0.lean_star : v0.lean;
     if (E > 0) {
         v.fn = h->output == 1 ? v0.epoch_star : v0.epoch;
         a.nchunks = (uint32_t)((iters + E - 1) / E);

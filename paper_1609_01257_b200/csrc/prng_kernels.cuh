@@ -516,6 +516,80 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- a2+a3, lean single-path form
+// batch_kernel instantiates several unit paths (full / partial pieces, idle trips, jump
+// starts), and ptxas allocates registers for all of them at once: in its hot loop it copies
+// the eight operands of every 32-B store into a staging octet (16 IMAD.MOV per iteration
+// at NPT = 8).  This kernel has one path only -- every piece full, natural order, no
+// chunks -- which the host guarantees before picking it (count % (32 NPT) == 0): the
+// ping-pong hot loop then needs 10 instead of 34 moves per two iterations at NPT = 8.
+// Every active warp of a CTA runs the same instructions, so the .aligned bar.sync is valid.
+template <int VEC, int NPT, int OUT = 0>
+__global__ void __launch_bounds__(256) batch_kernel_lean(BatchArgs a) {
+    static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
+    constexpr int NV = NPT / VEC;
+    constexpr uint64_t PIECE = 32ull * NPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t cta_warp0 = (uint64_t)blockIdx.x * wpb;
+    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
+    for (uint32_t r = 0; r < a.rounds; ++r) {
+        const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
+        const uint64_t unit = first + (warp - cta_warp0);
+        if (unit >= a.npieces) break;  // warp-uniform: a suffix of the CTA's warps
+        const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - first < wpb ? a.npieces - first : wpb);
+        const uint64_t base = unit * PIECE + (uint64_t)lane * VEC;
+        uint64_t x[NPT], y[NPT];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+        uint32_t slot = (uint32_t)(a.slot0 % a.nslots);
+        uint64_t *p = a.dst + (uint64_t)slot * a.pitch + base;
+        auto put = [&](const uint64_t *src) {  // store one iteration, barrier, next slot
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                if constexpr (OUT == 0) {
+                    store_vec<VEC, 0>(p + v * 32 * VEC, src + v * VEC);
+                } else {
+                    uint64_t z[VEC];
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) z[q] = emit<OUT>(src[v * VEC + q]);
+                    store_vec<VEC, 0>(p + v * 32 * VEC, z);
+                }
+            }
+            cta_barrier<true>(bar_threads);
+            if (++slot == a.nslots) {
+                slot = 0;
+                p -= wrap;
+            } else {
+                p += a.pitch;
+            }
+        };
+        uint32_t t = 0;
+        if (a.first_is_state && a.iters > 0) {  // iteration 0 of a run: the seeds themselves
+            put(x);
+            t = 1;
+        }
+#pragma unroll 1
+        for (; t + 1 < a.iters; t += 2) {  // the hot loop: ping-pong x -> y -> x
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) y[j] = xorshift64(x[j]);
+            put(y);
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(y[j]);
+            put(x);
+        }
+        if (t < a.iters) {
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
+            put(x);
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+    }
+}
+
 // ---------------------------------------------------------------- a2+a3, epoch-major order
 // L2 absorption: batch_kernel runs each piece through all T iterations of a
 // launch, so when a launch wraps a ring of R slots a warp rewrites its piece's R slots

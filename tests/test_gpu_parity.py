@@ -11,7 +11,7 @@ from workloads import RAGGED_N, SEED_PARITY, SPEC_GRID_I, SPEC_GRID_N, sample_po
 
 # variants compiled with the NEXT-3 scrambled-output instantiation (prng_engine.cu VS(...))
 STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1", "v4n16s1", "v2n32s1", "v4n8s1a", "v4n4s1a",
-              "v4n8s1p", "v4n4s1p")
+              "v4n8s1p", "v4n4s1p", "v4n8s1l", "v4n4s1l")
 
 
 def _kid(name):
@@ -631,6 +631,42 @@ def test_chunks_never_race_on_a_wrapping_ring(slots, chunk):
         assert np.array_equal(P.prng_read_state(h, n), want[-1])
     finally:
         P.prng_destroy(h)
+
+
+@pytest.mark.parametrize("out_kind", [0, 1])
+@pytest.mark.parametrize("kname", ["v4n8s1l", "v4n4s1l"])
+def test_lean_kernel(kname, out_kind):
+    """The lean single-path kernel (batch_kernel_lean: every piece full, natural order)
+    runs when numrn is a multiple of the piece size.  Even and odd iteration counts,
+    split calls (the first launch starts with the seeds, later ones with a step), end to
+    end and device only, both output transforms, and a grid with several rounds per warp,
+    vs the oracle."""
+    for n in (1 << 16, 3 * 1024 * 37):   # multiples of 32 x 8 numbers
+        i = 301
+        want = (oracle.stream_star if out_kind else oracle.stream)(n, i, SEED_PARITY)
+        state = oracle.stream(n, i, SEED_PARITY)[-1]
+        for calls in ([i], [1, 2, 150, 148]):
+            h = P.prng_create(n, SEED_PARITY)
+            try:
+                P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid(kname))
+                P.prng_set_option(h, P.PRNG_OPT_OUTPUT, out_kind)
+                P.prng_set_option(h, P.PRNG_OPT_GRID_WARPS, 40)
+                out = np.zeros((i, n), np.uint64)
+                sink = P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0)
+                P.prng_init(h)
+                for c in calls:
+                    P.prng_generate(h, c, P.SINK_COPY, sink)
+                assert np.array_equal(out, want), (n, calls)
+                assert np.array_equal(P.prng_read_state(h, n), state)
+                P.prng_init(h)  # device only through the ring (no wrap: 301 < slots)
+                for c in calls:
+                    P.prng_generate(h, c)
+                _, _, R, first, _ = P.prng_device_ring(h)
+                for k in (0, 1, i // 2, i - 1):
+                    assert np.array_equal(P.prng_read_slot(h, (first + k) % R, n), want[k]), k
+                assert np.array_equal(P.prng_read_state(h, n), state)
+            finally:
+                P.prng_destroy(h)
 
 
 @pytest.mark.parametrize("kname", STAR_NAMES)
