@@ -79,6 +79,8 @@ const Variant kVariants[] = {
     V("v4n8cs", 4, 8, 1, 0, 1, 0),    V("v2n8cs", 2, 8, 1, 0, 1, 0),
     // cluster barrier (split arrive / wait) every iteration (c2 ~ s1; c4 ~ 4.4 TB/s)
     V("v2n8c2", 2, 8, 0, 2, 2, 4),    V("v2n8c4", 2, 8, 0, 2, 4, 4),
+    // the bench geometry (32-B stores, 8 numbers per thread) with a 2-CTA cluster barrier
+    V("v4n8c2", 4, 8, 0, 2, 2, 4),
     // long per-CTA chunks: 32 / 64 numbers per thread (16 / 32 KiB per warp per iteration)
     // (measured: no gain over v2n4s1; 64 numbers/thread spills and was removed)
     VS("v2n32s1", 2, 32, 4),  V("v4n32s1", 4, 32, 0, 1, 1, 4),

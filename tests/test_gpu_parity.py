@@ -184,7 +184,7 @@ def test_autotune_then_parity():
     assert np.array_equal(out, oracle.stream(n, i, SEED_PARITY))
 
 
-@pytest.mark.parametrize("kv", range(48))
+@pytest.mark.parametrize("kv", range(56))
 def test_every_variant_device_only_wrapping_ring(kv):
     """Each kernel variant through the device-only ring path (grid-strided rounds, ring
     wrap-around inside one launch), vs the oracle at the ring slots and the state."""
