@@ -207,8 +207,17 @@ def ncu_traffic(variant, epoch):
         return None, None
     with open(p) as f:
         d = json.load(f)
-    want = f"batch_kernel<{m.group(1)}, {m.group(2)}, 0, 1, 0, {1 if m.group(3) else 0}>"  # ncu's spelling
-    if not any(want in k.get("kernel", "") for k in d.get("kernels", [])):
+    # ncu spells bools as 0/1; later template parameters (IL, PP) default to 0
+    want = [m.group(1), m.group(2), "0", "1", "0", "1" if m.group(3) else "0"]
+
+    def same_kernel(name):
+        mm = re.search(r"batch_kernel<([^>]*)>", name)
+        if not mm:
+            return False
+        args = [x.strip() for x in mm.group(1).split(",")]
+        return args[:6] == want and all(x in ("0", "false") for x in args[6:])
+
+    if not any(same_kernel(k.get("kernel", "")) for k in d.get("kernels", [])):
         return None, None
     return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
 
