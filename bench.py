@@ -93,7 +93,11 @@ class Dist:
 
     def barrier(self):
         if self.dist:
-            self.dist.barrier()
+            if self.dist.get_backend() == "nccl":  # name the device: no guess by NCCL
+                import torch
+                self.dist.barrier(device_ids=[torch.cuda.current_device()])
+            else:
+                self.dist.barrier()
 
     def max(self, x: float) -> float:
         if not self.dist:
