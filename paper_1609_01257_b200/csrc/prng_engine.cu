@@ -81,6 +81,10 @@ const Variant kVariants[] = {
     V("v2n8c2", 2, 8, 0, 2, 2, 4),    V("v2n8c4", 2, 8, 0, 2, 4, 4),
     // the bench geometry (32-B stores, 8 numbers per thread) with a 2-CTA cluster barrier
     V("v4n8c2", 4, 8, 0, 2, 2, 4),
+    // v4n8s1a with store cache policies: .cs, L2::evict_first hint, L1::no_allocate
+    {"v4n8s1a_cs", 4, 8, 1, 1, 1, 4, prngk::batch_kernel<4, 8, 1, 1, 0, true>, 0, nullptr, nullptr, nullptr},
+    {"v4n8s1a_ef", 4, 8, 2, 1, 1, 4, prngk::batch_kernel<4, 8, 2, 1, 0, true>, 0, nullptr, nullptr, nullptr},
+    {"v4n8s1a_na", 4, 8, 3, 1, 1, 4, prngk::batch_kernel<4, 8, 3, 1, 0, true>, 0, nullptr, nullptr, nullptr},
     // long per-CTA chunks: 32 / 64 numbers per thread (16 / 32 KiB per warp per iteration)
     // (measured: no gain over v2n4s1; 64 numbers/thread spills and was removed)
     VS("v2n32s1", 2, 32, 4),  V("v4n32s1", 4, 32, 0, 1, 1, 4),
