@@ -46,7 +46,7 @@ def lib():
         L.orc_xorshift64.argtypes, L.orc_xorshift64.restype = [u64], u64
         L.orc_sample.argtypes, L.orc_sample.restype = [u32, u64, u64], u64
         L.orc_stream.argtypes, L.orc_stream.restype = [u64, u64, u64, u64, u64, p64], i32
-        L.orc_digest.argtypes, L.orc_digest.restype = [u64, u64, u64, u64, u64, p64, p64], i32
+        L.orc_digest.argtypes, L.orc_digest.restype = [u64, u64, u64, u64, u64, p64, p64, p64, p64], i32
         L.orc_star.argtypes, L.orc_star.restype = [u64], u64
         L.orc_stream_star.argtypes, L.orc_stream_star.restype = [u64, u64, u64, u64, u64, p64], i32
         _lib = L
@@ -96,14 +96,29 @@ def stream_bytes(numrn: int, numiter: int, seed: int = 0) -> bytes:
 
 def digest(numrn: int, numiter: int, seed: int = 0, gid_begin: int = 0, count: int | None = None):
     """Per-iteration (xor, sum mod 2^64) folds of the outputs: two uint64[numiter] arrays."""
+    r = folds(numrn, numiter, seed, gid_begin, count)
+    return r["xor"], r["sum"]
+
+
+def folds(numrn: int, numiter: int, seed: int = 0, gid_begin: int = 0, count: int | None = None,
+          last: bool = False) -> dict:
+    """One pass of the flat loop: per-iteration xor, sum and gid-weighted sum
+    (sum of (2 g + 1) out[k][g] mod 2^64, g global) as uint64[numiter] arrays, plus
+    (last=True) the final iteration out[numiter-1][gid_begin:gid_begin+count]."""
     if count is None:
         count = numrn - gid_begin
     x = np.empty(numiter, dtype=np.uint64)
     s = np.empty(numiter, dtype=np.uint64)
-    rc = lib().orc_digest(numrn, numiter, seed & 0xFFFFFFFFFFFFFFFF, gid_begin, count, _p64(x), _p64(s))
+    w = np.empty(numiter, dtype=np.uint64)
+    lo = np.empty(count if last else 0, dtype=np.uint64)
+    rc = lib().orc_digest(numrn, numiter, seed & 0xFFFFFFFFFFFFFFFF, gid_begin, count, _p64(x), _p64(s), _p64(w),
+                          _p64(lo) if last else None)
     if rc != 0:
         raise ValueError(f"orc_digest rc={rc}")
-    return x, s
+    out = {"xor": x, "sum": s, "wsum": w}
+    if last:
+        out["last"] = lo
+    return out
 
 
 def star(x: int) -> int:

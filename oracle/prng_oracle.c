@@ -135,12 +135,20 @@ int orc_stream(uint64_t numrn, uint64_t numiter, uint64_t seed,
     return ORC_OK;
 }
 
-/* The same flat loop, folding each iteration's `count` outputs into an XOR and
- * a wrapping sum instead of storing them (the large-run parity digests,
- * SURVEY.md §8(c) "Parity procedure").  xor_out / sum_out hold numiter words. */
+/* The same flat loop, folding each iteration's `count` outputs instead of storing them
+ * (the large-run parity digests, SURVEY.md §8(c) "Parity procedure"), with every output
+ * optional (NULL = not wanted):
+ *   xor_out[k]  = XOR over g of out[k][g]
+ *   sum_out[k]  = SUM over g of out[k][g]                mod 2^64
+ *   wsum_out[k] = SUM over g of (2*g + 1) * out[k][g]    mod 2^64, g the GLOBAL gid --
+ *                 position-weighted, so it changes when outputs swap places (the XOR and
+ *                 the sum do not); the odd weights make each term a bijection of out[k][g]
+ *   last_out[j] = out[numiter-1][gid_begin + j]          (the final state of the loop)
+ * xor / sum / wsum hold numiter words, last_out count words. */
 int orc_digest(uint64_t numrn, uint64_t numiter, uint64_t seed,
                uint64_t gid_begin, uint64_t count,
-               uint64_t *xor_out, uint64_t *sum_out)
+               uint64_t *xor_out, uint64_t *sum_out, uint64_t *wsum_out,
+               uint64_t *last_out)
 {
     int rc = orc_check(numrn, numiter, gid_begin, count);
     if (rc != ORC_OK)
@@ -149,19 +157,28 @@ int orc_digest(uint64_t numrn, uint64_t numiter, uint64_t seed,
     if (!s)
         return ORC_ENOMEM;
     for (uint64_t k = 0; k < numiter; ++k) {
-        uint64_t fx = 0, fs = 0;
+        uint64_t fx = 0, fs = 0, fw = 0;
         for (uint64_t j = 0; j < count; ++j) {
-            uint32_t g = (uint32_t)(gid_begin + j);
+            uint64_t gid = gid_begin + j;
+            uint32_t g = (uint32_t)gid;
             if (k == 0)
                 s[j] = orc_seed64(g, seed);
             else
                 s[j] = orc_xorshift64(s[j]);
             fx ^= s[j];
             fs += s[j];
+            fw += (2 * gid + 1) * s[j];
         }
-        xor_out[k] = fx;
-        sum_out[k] = fs;
+        if (xor_out)
+            xor_out[k] = fx;
+        if (sum_out)
+            sum_out[k] = fs;
+        if (wsum_out)
+            wsum_out[k] = fw;
     }
+    if (last_out)
+        for (uint64_t j = 0; j < count; ++j)
+            last_out[j] = s[j];
     free(s);
     return ORC_OK;
 }

@@ -318,3 +318,91 @@ def test_star_multiplier_is_vignas_and_invertible():
     back = (t.astype(object) * inv) % (1 << 64)
     assert np.array_equal(back.astype(np.uint64), s)
     assert oracle.star(1) == M
+
+
+# ---------------------------------------------------------------- A3: the zero-state fix-up
+def _fmix64_inverse(y):
+    """Inverse of the A4 premix, from the algebra: x ^ (x >> 33) is an involution on u64
+    (33 >= 32) and the two odd multipliers are undone by their inverses mod 2^64."""
+    def unx33(v):
+        return v ^ (v >> 33)
+    y = unx33(y)
+    y = (y * pow(0xC4CEB9FE1A85EC53, -1, 1 << 64)) & M64
+    y = unx33(y)
+    y = (y * pow(0xFF51AFD7ED558CCD, -1, 1 << 64)) & M64
+    return unx33(y)
+
+
+def _a3_trigger():
+    """A (gid, seed) whose raw composition is 0 ("if result is 0, substitute
+    1"; PAPER.md P:173 needs nonzero seeds).  seed64 is 0 iff wang32(g ^ a) = 0 and
+    wang32(g ^ C ^ b) = 0 with (a, b) = (lo32, hi32) of fmix64(seed) and C = 0x9E3779B9,
+    i.e. g ^ a = g ^ C ^ b = w0 := wang32^-1(0).  Take a = C, b = 0: fmix64(seed) = C and
+    g = w0 ^ C -- derived with the two algebraic inverses, never from the oracle."""
+    C = 0x9E3779B9
+    w0 = _wang32_inverse(0)
+    return w0 ^ C, _fmix64_inverse(C)
+
+
+def test_a3_zero_fixup_trigger():
+    """A3: the zero -> 1 fix-up fires at the derived trigger, and only the A3 branch can make
+    it 1: the raw composition there is 0 (both hashes 0).  Catches a dropped fix-up (0), a
+    wrong substitute (0 -> gid, 0 -> anything else) and a fix-up applied to nonzero states.
+    The trigger matches the one VERDICT r1 derived independently."""
+    g, s = _a3_trigger()
+    assert (g, s) == (2654435716, 0x236D2904C6FC2D12)
+    assert _fmix64_inverse(oracle.fmix64(s)) == s and oracle.fmix64(s) == 0x9E3779B9
+    m = oracle.fmix64(s)
+    a, b = m & M32, m >> 32
+    assert oracle.wang32(g ^ a) == 0 and oracle.wang32(g ^ 0x9E3779B9 ^ b) == 0   # raw composition = 0
+    assert oracle.seed64(g, s) == 1
+    # neighbours are untouched: their raw composition is nonzero and emitted as is
+    for gg in (g - 1, g + 1):
+        raw = (oracle.wang32(gg ^ a) << 32) | oracle.wang32(gg ^ 0x9E3779B9 ^ b)
+        assert raw != 0 and oracle.seed64(gg, s) == raw
+    # the stream from the fixed-up state is xs^k(1): 1, xs(1) = 1082269761 (S:485), ...
+    st = oracle.stream(1 << 32, 3, s, gid_begin=g - 1, count=3)
+    assert st[0, 1] == 1 and st[1, 1] == 1082269761 and st[2, 1] == oracle.xorshift64(1082269761)
+    r = oracle.folds(1 << 32, 1, s, gid_begin=g, count=1, last=True)
+    assert r["last"][0] == 1 and r["xor"][0] == 1 and r["wsum"][0] == 2 * g + 1
+
+
+# ---------------------------------------------------------------- folds: position-weighted digest, last row
+def test_folds_weighted_sum_by_hand(golden):
+    """The gid-weighted fold sum_g (2 g + 1) out[k][g] mod 2^64 against hand arithmetic on the
+    SURVEY App. A states (n = 4, k = 0..3): catches a wrong weight, an unweighted sum, or
+    weights from the handle-relative instead of the global gid."""
+    g = golden("survey_appendix_a.json")["states_seed0"]
+    st = [[int(v, 16) for v in g[str(gid)]] for gid in range(4)]
+    r = oracle.folds(4, 4, 0)
+    for k in range(4):
+        assert int(r["wsum"][k]) == sum((2 * gid + 1) * st[gid][k] for gid in range(4)) & M64
+        assert int(r["sum"][k]) == sum(st[gid][k] for gid in range(4)) & M64
+    # a sub-range weighs by the global gid: gids 2..3 only
+    r2 = oracle.folds(4, 4, 0, gid_begin=2, count=2)
+    for k in range(4):
+        assert int(r2["wsum"][k]) == (5 * st[2][k] + 7 * st[3][k]) & M64
+
+
+def test_folds_weighted_sum_sees_a_swap():
+    """The reason for the weighted fold: swapping two outputs of one iteration leaves the
+    XOR and the sum unchanged but changes sum (2 g + 1) x (by 2 (a - b)(x_b - x_a))."""
+    s = oracle.stream(1000, 2, 5)[1].astype(object)
+    w = [2 * g + 1 for g in range(1000)]
+    t = list(s)
+    t[10], t[900] = t[900], t[10]
+    assert sum(s) % (1 << 64) == sum(t) % (1 << 64)
+    assert sum(a * b for a, b in zip(w, s)) % (1 << 64) != sum(a * b for a, b in zip(w, t)) % (1 << 64)
+
+
+def test_folds_last_row_and_config1(golden):
+    """last = the final iteration (App. A k = 3 column at n = 4, i = 4; the config-1 last word
+    for 3 seeds), and the per-iteration folds combine to App. A's whole-stream XOR / sum."""
+    g = golden("survey_appendix_a.json")
+    assert [int(x) for x in oracle.folds(4, 4, 0, last=True)["last"]] == \
+        [int(g["states_seed0"][str(gid)][3], 16) for gid in range(4)]
+    for seed_s, d in g["config1_n1024_i8"].items():
+        r = oracle.folds(1024, 8, int(seed_s), last=True)
+        assert int(r["last"][-1]) == int(d["last"], 16)
+        assert int(np.bitwise_xor.reduce(r["xor"])) == int(d["xor"], 16)
+        assert int(r["sum"].sum(dtype=np.uint64)) == int(d["sum"], 16)
