@@ -22,9 +22,13 @@ random numbers/s (and GB/s, 8 B per number, Eq. 1) device-only and end to end.
              against MEASURED_PEAKS.json hbm_gbs.
 * cpu_baseline  the oracle (oracle/, plain single-threaded C) on a bounded sample.
 
-Rank r of N owns the contiguous gid range shard_range(numrn_total, r, N) (weak scaling:
-numrn per GPU fixed, default 2^24).  The only collectives are a barrier and a MAX
-all-reduce of the elapsed times.
+Workloads (BASELINE.json configs, `workload()` below):
+* N = 1: device-only config 2 (numrn = 2^24, numiter = 1000); e2e config 3 (same shape).
+* N > 1: device-only config 4 (numrn = 2^28 TOTAL, gid-range sharded, numiter = 1000:
+  strong scaling); e2e config 5 (2^28 total, numiter = 100, per-rank D2H).  The e2e host
+  link roofline at N > 1 is the all-ranks-concurrent pinned D2H probe (barrier-synchronised).
+Rank r of N owns the contiguous gid range shard_range(numrn_total, r, N).  The only
+collectives are barriers and MAX / SUM all-reduces of timings and probe results.
 """
 from __future__ import annotations
 
@@ -47,8 +51,59 @@ METRIC_DETAIL = "value: device-only random numbers/s (gbs = 8 B/number); e2e: sa
 from workloads import SEED_PERF, shard_range  # noqa: E402
 
 HBM_THEORETICAL_GBS = 8 * 1024 / 8 * 2 * 3.996  # 8 HBM3e stacks x 1024 bit x 2 x 3996 MHz
-DEF_NUMRN = 1 << 24
-DEF_NUMITER = 1000
+DEF_NUMRN = 1 << 24          # BASELINE configs 2 / 3 (one GPU)
+DEF_NUMRN_MULTI = 1 << 28    # BASELINE configs 4 / 5 (total over N > 1 GPUs)
+DEF_NUMITER = 1000           # configs 2 / 3 / 4
+DEF_NUMITER_C5 = 100         # config 5 (e2e at N > 1)
+REF_SAMPLE_ITERS = 64        # reference arm / cpu_baseline: iterations per sampled step
+REF_SAMPLE_GIDS = 1 << 24    # ... over at most this many gids of the workload
+
+
+def workload(numrn_total: int, numiter: int, e2e_numiter: int, world: int) -> dict:
+    """The BASELINE.json config bench.py measures at `world` GPUs (0 = that config's
+    default): device-only config 2 at N = 1, config 4 at N > 1 (strong scaling over a fixed
+    2^28 total); end to end config 3 at N = 1, config 5 at N > 1."""
+    multi = world > 1
+    n = numrn_total or (DEF_NUMRN_MULTI if multi else DEF_NUMRN)
+    it = numiter or DEF_NUMITER
+    e2e_it = e2e_numiter or (DEF_NUMITER_C5 if multi else it)
+    per = n // world
+    lg = n.bit_length() - 1
+    nstr = f"2^{lg}" if n == 1 << lg else str(n)
+    if multi:
+        dev = (f"BASELINE config 4: numrn={nstr} total per iteration, gid-range sharded over {world} GPUs "
+               f"({per} per GPU) x numiter={it}, device-only")
+        e2e = (f"BASELINE config 5: numrn={nstr} total, gid-range sharded over {world} GPUs x numiter={e2e_it}, "
+               f"end to end with per-rank D2H overlap")
+    else:
+        dev = f"BASELINE config 2: numrn={nstr} ({n}) per iteration x numiter={it}, device-only"
+        e2e = (f"BASELINE config 3: numrn={nstr} x numiter={e2e_it}, end to end with double-buffered D2H into "
+               f"pinned host memory")
+    if numrn_total and n != (DEF_NUMRN_MULTI if multi else DEF_NUMRN) or numiter and it != DEF_NUMITER:
+        dev = dev.replace("BASELINE config", "off-BASELINE shape (cf. config")
+    return {"numrn": n, "numiter": it, "e2e_numiter": e2e_it, "workload": dev, "e2e_workload": e2e,
+            # N > 1 splits a fixed 2^28 total (config 4); N = 1 is config 2's one-GPU shape
+            "scaling": "strong", "per_gpu": per}
+
+
+def cpu_model() -> str:
+    """The host CPU model (lscpu "Model name", else /proc/cpuinfo), for the baseline lines."""
+    import subprocess
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.strip().startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def parse():
@@ -57,9 +112,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--numrn-per-gpu", type=int, default=DEF_NUMRN)
-    ap.add_argument("--numrn-total", type=int, default=0, help="strong scaling: fixed total numrn (e.g. 2^28)")
-    ap.add_argument("--numiter", type=int, default=DEF_NUMITER)
+    ap.add_argument("--numrn-total", type=int, default=0,
+                    help="total numrn per iteration (0 = the BASELINE config: 2^24 at N = 1, 2^28 at N > 1)")
+    ap.add_argument("--numiter", type=int, default=0, help="device-only numiter (0 = 1000)")
+    ap.add_argument("--e2e-numiter", type=int, default=0, help="end-to-end numiter (0 = 1000 at N = 1, 100 at N > 1)")
+    ap.add_argument("--sustained-steps", type=int, default=100,
+                    help="device-only steps of the sustained (power-capped) figure after the timed region; 0 = off")
     ap.add_argument("--seed", type=int, default=SEED_PERF)
     ap.add_argument("--kernel", type=int, default=0, help="kernel variant id (default 0 = auto: v4n8s1 at the bench shape; -1: prng_autotune)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -68,8 +126,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probes", action="store_true")
-    ap.add_argument("--cpu-numiter", type=int, default=64, help="oracle sample: numiter at full numrn")
-    ap.add_argument("--ref-numiter", type=int, default=8, help="--impl reference: numiter per step sample")
+    ap.add_argument("--cpu-numiter", type=int, default=REF_SAMPLE_ITERS, help="oracle sample: iterations")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--output", type=int, default=0, help="0 = the state (paper); 1 = xorshift64* scrambled (NEXT-3)")
     ap.add_argument("--no-numa-bind", action="store_true", help="keep the process's CPU affinity")
@@ -107,6 +164,20 @@ class Dist:
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
+
+    def min(self, x: float) -> float:
+        return -self.max(-x)
+
+    def gather(self, x: float) -> list:
+        """Every rank's value, in rank order (an all-reduce SUM of one-hot vectors)."""
+        if not self.dist:
+            return [x]
+        import torch
+        dev = "cuda" if self.dist.get_backend() == "nccl" else "cpu"
+        t = torch.zeros(self.world, dtype=torch.float64, device=dev)
+        t[self.rank] = x
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return [float(v) for v in t.tolist()]
 
     def close(self):
         if self.dist:
@@ -203,23 +274,23 @@ def measured_peaks():
 
 def ncu_traffic(variant, epoch):
     """Per-launch DRAM bytes of the batch kernel from the committed ncu --set full summary,
-    if that capture is of this kernel (variant "v{VEC}n{NPT}s1[a]", natural order)."""
+    if that capture is of this kernel (variant "v{VEC}n{NPT}s1[a|p]", natural order)."""
     import re
     p = os.path.join(ROOT, "profiles", "ncu_batch_kernel.json")
-    m = re.fullmatch(r"v(\d+)n(\d+)s1(a?)", variant or "")
+    m = re.fullmatch(r"v(\d+)n(\d+)s1([ap]?)", variant or "")
     if not os.path.exists(p) or not m or epoch:
         return None, None
     with open(p) as f:
         d = json.load(f)
-    # ncu spells bools as 0/1; later template parameters (IL, PP) default to 0
-    want = [m.group(1), m.group(2), "0", "1", "0", "1" if m.group(3) else "0"]
+    # batch_kernel<VEC, NPT, OUT, AL, PP>; ncu spells bools as true/false or 1/0
+    want = [m.group(1), m.group(2), "0", "1" if m.group(3) == "a" else "0", "1" if m.group(3) == "p" else "0"]
 
     def same_kernel(name):
         mm = re.search(r"batch_kernel<([^>]*)>", name)
         if not mm:
             return False
-        args = [x.strip() for x in mm.group(1).split(",")]
-        return args[:6] == want and all(x in ("0", "false") for x in args[6:])
+        args = [x.strip().replace("true", "1").replace("false", "0") for x in mm.group(1).split(",")]
+        return args == want
 
     if not any(same_kernel(k.get("kernel", "")) for k in d.get("kernels", [])):
         return None, None
@@ -227,22 +298,21 @@ def ncu_traffic(variant, epoch):
 
 
 # ---------------------------------------------------------------- oracle timing (CPU)
-def cpu_baseline(numrn, numiter, seed):
+def cpu_baseline(numrn, count, numiter, seed):
     import oracle
     t = time.perf_counter()
-    oracle.digest(numrn, numiter, seed)
+    oracle.digest(numrn, numiter, seed, 0, count)
     dt = time.perf_counter() - t
-    return numrn * numiter / dt, dt
+    return count * numiter / dt, dt
 
 
-def cpu_baseline_all_cores(numrn, numiter, seed):
+def cpu_baseline_all_cores(numrn, count, numiter, seed):
     """The same oracle function, unchanged, on one contiguous gid shard per host core
     (threads: ctypes releases the GIL), as BASELINE.md's CPU plan asks."""
-    import threading
     import oracle
     cores = len(os.sched_getaffinity(0))
     oracle.lib()
-    shards = [shard_range(numrn, r, cores) for r in range(cores)]
+    shards = [shard_range(count, r, cores) for r in range(cores)]
     th = [threading.Thread(target=oracle.digest, args=(numrn, numiter, seed, b, c)) for b, c in shards if c]
     t = time.perf_counter()
     for x in th:
@@ -250,37 +320,51 @@ def cpu_baseline_all_cores(numrn, numiter, seed):
     for x in th:
         x.join()
     dt = time.perf_counter() - t
-    return numrn * numiter / dt, dt, len(th)
+    return count * numiter / dt, dt, len(th)
+
+
+def ref_sample(numrn):
+    """The bounded oracle sample of a workload: the first min(numrn, 2^24) gids over
+    REF_SAMPLE_ITERS iterations (seeding is 1/64 of it; numbers/s is flat in numiter)."""
+    return min(numrn, REF_SAMPLE_GIDS), REF_SAMPLE_ITERS
 
 
 def run_reference(a, D):
-    """--impl reference: the oracle as it stands, on the host cores, rank 0 only."""
+    """--impl reference: the oracle as it stands (plain single-threaded C), on the host cores,
+    rank 0 only, each step a bounded sample of the same workload as our arm."""
     if D.rank != 0:
         return
     import oracle
     oracle.build()
-    numrn = a.numrn_total or a.numrn_per_gpu * D.world
-    ni = a.ref_numiter
+    W = workload(a.numrn_total, a.numiter, a.e2e_numiter, D.world)
+    numrn = W["numrn"]
+    cnt, ni = ref_sample(numrn)
     for _ in range(a.warmup):
-        oracle.digest(numrn, ni, a.seed)
+        oracle.digest(numrn, ni, a.seed, 0, cnt)
     t = time.perf_counter()
     for _ in range(a.steps):
-        oracle.digest(numrn, ni, a.seed)
+        oracle.digest(numrn, ni, a.seed, 0, cnt)
     dt = time.perf_counter() - t
-    v = numrn * ni * a.steps / dt
-    sample = f"numrn={numrn} x numiter={ni} per step (of the workload's numiter={a.numiter}); digest-folded"
+    v = cnt * ni * a.steps / dt
+    sample = (f"gids [0, {cnt}) of numrn={numrn} x numiter={ni} per step (of the workload's numiter={W['numiter']}); "
+              f"the flat loop folded into per-iteration digests, 1 thread")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "metric_detail": METRIC_DETAIL, "value": v,
         "unit": "numbers/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"numrn={numrn}, numiter={a.numiter}, seed={a.seed} (sampled)"},
-        "cpu_baseline": {"value": v, "unit": "numbers/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": W["scaling"],
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (numrn, numiter, seed)",
+        "config": {"workload": W["workload"], "numrn": numrn, "numiter": W["numiter"], "seed": a.seed,
+                   "sampled": True},
+        "cpu_baseline": {"value": v, "unit": "numbers/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
+                         "sample": sample},
         "e2e": {"value": v, "unit": "numbers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
 # ---------------------------------------------------------------- our arm
+BAD_CLOCK_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "hw_power_brake_slowdown"}
+
+
 def run_ours(a, D):
     import torch
     import paper_1609_01257_b200 as P
@@ -288,7 +372,8 @@ def run_ours(a, D):
     dev = D.local % a.device_mod if a.device_mod > 0 else D.local
     torch.cuda.set_device(dev)
     numa = bind_to_gpu_cpus(dev) if not a.no_numa_bind else None
-    numrn = a.numrn_total or a.numrn_per_gpu * D.world
+    W = workload(a.numrn_total, a.numiter, a.e2e_numiter, D.world)
+    numrn, numiter, e2e_numiter = W["numrn"], W["numiter"], W["e2e_numiter"]
     gb, cnt = shard_range(numrn, D.rank, D.world)
     gen = torch.cuda.Stream()
     cop = torch.cuda.Stream()
@@ -302,60 +387,71 @@ def run_ours(a, D):
         tune_gbs = P.prng_autotune(h)
     else:
         P.prng_set_option(h, P.PRNG_OPT_KERNEL, a.kernel)
-    kernel = P.prng_get_option(h, P.PRNG_OPT_KERNEL)
     grid_warps = P.prng_get_option(h, P.PRNG_OPT_GRID_WARPS)
 
     # ---- device only
     for _ in range(a.warmup):
         P.prng_init(h)
-        P.prng_generate(h, a.numiter)
+        P.prng_generate(h, numiter)
+
     # Timed region: K steps enqueued back to back on the generation stream (no host round
     # trips between steps: PRNG_OPT_BLOCKING 0), per-launch CUDA-event intervals accumulated
     # (PRNG_OPT_PROFILE 2) and read after the region.
-    def timed_region():
-        P.prng_set_option(h, P.PRNG_OPT_PROFILE, 2)
+    def timed_region(steps, profile=True):
+        if profile:
+            P.prng_set_option(h, P.PRNG_OPT_PROFILE, 2)
         P.prng_set_option(h, P.PRNG_OPT_BLOCKING, 0)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with Clocks(dev) as clk:
             D.barrier()
             torch.cuda.synchronize()
             ev0.record(gen)
-            for _ in range(a.steps):
+            for _ in range(steps):
                 P.prng_init(h)
-                P.prng_generate(h, a.numiter)
+                P.prng_generate(h, numiter)
             ev1.record(gen)
             torch.cuda.synchronize()
             D.barrier()
         P.prng_set_option(h, P.PRNG_OPT_BLOCKING, 1)
-        ids, s, e, _ = P.prng_prof_events(h)  # per-launch CUDA-event intervals of the K steps
-        P.prng_set_option(h, P.PRNG_OPT_PROFILE, 0)
+        ids = s = e = None
+        if profile:
+            ids, s, e, _ = P.prng_prof_events(h)  # per-launch CUDA-event intervals of the K steps
+            P.prng_set_option(h, P.PRNG_OPT_PROFILE, 0)
         return ev0.elapsed_time(ev1), ids, s, e, clk.summary()
 
-    ms, ids, s, e, clocks = timed_region()
-    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "hw_power_brake_slowdown"}
+    ms, ids, s, e, clocks = timed_region(a.steps)
     # the contract: a run that saw these is rejected and re-measured once (decided jointly:
     # every rank takes part in the barriers of the re-run)
-    if D.max(1.0 if bad & set(clocks["reasons"]) else 0.0) > 0:
+    if D.max(1.0 if BAD_CLOCK_REASONS & set(clocks["reasons"]) else 0.0) > 0:
         first = clocks
-        ms, ids, s, e, clocks = timed_region()
+        ms, ids, s, e, clocks = timed_region(a.steps)
         clocks["remeasured_after"] = first["reasons"]
     kern_ms = [1e3 * (y - x) for i, x, y in zip(ids, s, e) if i == 1]
     init_ms = [1e3 * (y - x) for i, x, y in zip(ids, s, e) if i == 0]
     launches = len(ids)
     ms_max = D.max(ms)
-    numbers = numrn * a.numiter * a.steps
-    value = numbers / (ms_max * 1e-3)
+    value = numrn * numiter * a.steps / (ms_max * 1e-3)
+
+    sustained = None
+    if a.sustained_steps > 0:  # the same step back to back for seconds: the power-capped rate
+        sms, _, _, _, sclk = timed_region(a.sustained_steps, profile=False)
+        sms_max = D.max(sms)
+        sustained = {"value": numrn * numiter * a.sustained_steps / (sms_max * 1e-3), "unit": "numbers/s",
+                     "gbs": 8 * numrn * numiter * a.sustained_steps / (sms_max * 1e-3) / 1e9,
+                     "steps": a.sustained_steps, "ms_per_step": sms_max / a.sustained_steps, "clocks": sclk,
+                     "note": "not the headline: the same device-only step repeated for seconds, at the clock the "
+                             "1 kW power cap settles to"}
 
     peak, peak_src = measured_peaks()
     kmean = statistics.mean(kern_ms)
-    algo_bytes = 8 * cnt * a.numiter
+    algo_bytes = 8 * cnt * numiter
     achieved = algo_bytes / (kmean * 1e-3) / 1e9
     ran, epoch = P.prng_last_launch(h)  # the kernel the timed launches ran ("auto", anti-absorption)
-    traffic, traffic_algo = ncu_traffic(P.prng_kernel_variant_name(ran), epoch)
+    vname = P.prng_kernel_variant_name(ran)
+    traffic, traffic_algo = ncu_traffic(vname, epoch)
     if traffic_algo is not None and int(traffic_algo) != algo_bytes:
         traffic = None  # the committed capture is of another shape
-    kname = ("prngk::batch_kernel_epoch<" + P.prng_kernel_variant_name(ran) + f", E={epoch}>" if epoch else
-             "prngk::batch_kernel<" + P.prng_kernel_variant_name(ran) + ">")
+    kname = ("prngk::batch_kernel_epoch<" + vname + f", E={epoch}>" if epoch else "prngk::batch_kernel<" + vname + ">")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kname,
                 "grid_warps": grid_warps or "variant default", "autotune_probe_gbs": tune_gbs,
@@ -366,37 +462,38 @@ def run_ours(a, D):
                 "note": "write-only stream: the copy-based peak pays read/write turnarounds a pure write "
                         "stream does not; theoretical = 8 stacks x 1024 bit x 7.992 Gb/s = 8184 GB/s"}
 
-    # ---- end to end (host buffers, D2H inside the timed region)
+    # ---- end to end (host buffers, D2H inside the timed region): config 3 / config 5
     e2e = None
     if not a.no_e2e:
         for _ in range(a.e2e_warmup):
             P.prng_init(h)
-            P.prng_generate(h, a.numiter, P.SINK_NULL)
+            P.prng_generate(h, e2e_numiter, P.SINK_NULL)
         walls = []
         for _ in range(a.e2e_steps):
             D.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             P.prng_init(h)
-            P.prng_generate(h, a.numiter, P.SINK_NULL)
+            P.prng_generate(h, e2e_numiter, P.SINK_NULL)
             torch.cuda.synchronize()
             walls.append(time.perf_counter() - t0)
         # one more, untimed, step with per-batch CUDA-event intervals for the a6 overlap report
         P.prng_set_option(h, P.PRNG_OPT_PROFILE, 1)
         P.prng_init(h)
-        P.prng_generate(h, a.numiter, P.SINK_NULL)
+        P.prng_generate(h, e2e_numiter, P.SINK_NULL)
         prof = P.prng_prof_events(h)
         P.prng_set_option(h, P.PRNG_OPT_PROFILE, 0)
         wall = D.max(sum(walls))
-        ev = numrn * a.numiter * a.e2e_steps / wall
-        ids, s, e, w = prof
-        calc = P.prng_prof_calc(ids, s, e, 4)
+        ev = numrn * e2e_numiter * a.e2e_steps / wall
+        pids, ps, pe, w = prof
+        calc = P.prng_prof_calc(pids, ps, pe, 4)
         agg = calc["agg"]
         ov = calc["overlap"]
-        d2h_gbs = 8 * cnt * a.numiter * a.e2e_steps / sum(walls) / 1e9
+        d2h_gbs = 8 * cnt * e2e_numiter * a.e2e_steps / sum(walls) / 1e9
         e2e = {"value": ev, "unit": "numbers/s", "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": 8 * numrn * a.numiter, "gbs": 8 * ev / 1e9,
-               "mode": ["S0", "S1", "O1", "O2", "O3"][a.e2e_mode], "d2h_gbs_per_gpu": d2h_gbs,
+               "d2h_bytes_per_step": 8 * numrn * e2e_numiter, "gbs": 8 * ev / 1e9, "workload": W["e2e_workload"],
+               "numiter": e2e_numiter, "mode": ["S0", "S1", "O1", "O2", "O3"][a.e2e_mode],
+               "d2h_gbs_per_gpu": d2h_gbs, "d2h_gbs_per_gpu_min": D.min(d2h_gbs),
                "profile_extra_step": {
                    "rng_kernel_s": agg[1], "read_buffer_s": agg[2], "out_s": agg[3], "init_s": agg[0],
                    "rng_read_overlap_s": ov[1, 2],
@@ -409,40 +506,57 @@ def run_ours(a, D):
         rows = 2 * T
         harr = torch.empty((rows, cnt), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
         P.prng_init(h)
-        P.prng_generate_host(h, min(a.numiter, rows), harr, cnt, rows)  # warm-up
+        P.prng_generate_host(h, min(e2e_numiter, rows), harr, cnt, rows)  # warm-up
         D.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         P.prng_init(h)
-        P.prng_generate_host(h, a.numiter, harr, cnt, rows)
+        P.prng_generate_host(h, e2e_numiter, harr, cnt, rows)
         dt = D.max(time.perf_counter() - t0)
-        e2e["host_array"] = {"value": numrn * a.numiter / dt, "unit": "numbers/s",
-                             "gbs": 8 * numrn * a.numiter / dt / 1e9, "rows": rows,
+        e2e["host_array"] = {"value": numrn * e2e_numiter / dt, "unit": "numbers/s",
+                             "gbs": 8 * numrn * e2e_numiter / dt / 1e9, "rows": rows,
                              "how": "prng_generate_host: D2H straight into a pinned host array (ring of rows)"}
         del harr
-    probes = None
-    if not a.no_probes and D.rank == 0:
-        probes = {"memset_write_gbs": P.prng_probe_memset_gbs(32 << 30, 3),
-                  "store_kernel_write_gbs": P.prng_probe_store_gbs(32 << 30, 3),
-                  "d2h_pinned_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 1),
-                  "d2h_pinned_2streams_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 2)}
-        roofline["frac_of_same_box_memset"] = achieved / probes["memset_write_gbs"]
-        roofline["frac_of_same_box_store_kernel"] = achieved / probes["store_kernel_write_gbs"]
-        if e2e:
-            e2e["roofline"] = {"bound": "host-link", "achieved": e2e["d2h_gbs_per_gpu"],
-                               "peak": probes["d2h_pinned_gbs"], "unit": "GB/s",
-                               "frac": e2e["d2h_gbs_per_gpu"] / probes["d2h_pinned_gbs"],
-                               "peak_source": "same-box pinned cudaMemcpyAsync D2H 1 GiB, best of 5"}
     P.prng_destroy(h)
+
+    # ---- same-box denominators
+    probes = None
+    if not a.no_probes:
+        # the host link with every rank copying at once (barrier-synchronised, sustained):
+        # the e2e roofline's denominator, per rank and in aggregate
+        D.barrier()
+        link = P.prng_probe_d2h_sustained_gbs(1 << 30, 8)
+        D.barrier()
+        per_rank = D.gather(link)
+        probes = {"d2h_pinned_concurrent_gbs_per_rank": per_rank,
+                  "d2h_pinned_concurrent_gbs_aggregate": sum(per_rank)}
+        if D.rank == 0:
+            probes.update({"memset_write_gbs": P.prng_probe_memset_gbs(32 << 30, 3),
+                           "fill_kernel_write_gbs": P.prng_probe_fill_gbs(32 << 30, 3),
+                           "store_kernel_write_gbs": P.prng_probe_store_gbs(32 << 30, 3),
+                           "d2h_pinned_alone_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 1)})
+            roofline["frac_of_same_box_memset"] = achieved / probes["memset_write_gbs"]
+            roofline["frac_of_same_box_fill_kernel"] = achieved / probes["fill_kernel_write_gbs"]
+            roofline["frac_of_same_box_store_kernel"] = achieved / probes["store_kernel_write_gbs"]
+            if e2e:
+                agg_gbs = 8 * numrn * e2e_numiter * a.e2e_steps / wall / 1e9
+                e2e["roofline"] = {
+                    "bound": "host-link", "achieved": agg_gbs, "peak": probes["d2h_pinned_concurrent_gbs_aggregate"],
+                    "unit": "GB/s", "frac": agg_gbs / probes["d2h_pinned_concurrent_gbs_aggregate"],
+                    "per_rank_frac_min": min(e2e["d2h_gbs_per_gpu_min"] / x for x in per_rank),
+                    "peak_source": f"all {D.world} rank(s) at once: pinned cudaMemcpyAsync D2H, 8 x 1 GiB back to "
+                                   f"back per rank after a barrier, summed over ranks"}
 
     cpu = None
     if D.rank == 0 and D.world == 1 and not a.no_cpu:
-        v, dt = cpu_baseline(numrn, a.cpu_numiter, a.seed)
-        cpu = {"value": v, "unit": "numbers/s", "cores": 1, "kind": "oracle",
-               "sample": f"numrn={numrn} x numiter={a.cpu_numiter} ({dt:.1f} s, digest-folded, 1 thread)"}
-        va, dta, nth = cpu_baseline_all_cores(numrn, 4 * a.cpu_numiter, a.seed)
-        cpu["all_cores"] = {"value": va, "unit": "numbers/s", "cores": nth,
-                            "sample": f"numrn={numrn} x numiter={4 * a.cpu_numiter} ({dta:.1f} s), one gid shard "
+        ccnt, cni = ref_sample(numrn)
+        v, dt = cpu_baseline(numrn, ccnt, a.cpu_numiter, a.seed)
+        cpu = {"value": v, "unit": "numbers/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
+               "sample": f"gids [0, {ccnt}) of numrn={numrn} x numiter={a.cpu_numiter} ({dt:.1f} s, digest-folded, "
+                         f"1 thread): the same sample as --impl reference"}
+        va, dta, nth = cpu_baseline_all_cores(numrn, ccnt, 4 * a.cpu_numiter, a.seed)
+        cpu["all_cores"] = {"value": va, "unit": "numbers/s", "cores": nth, "cpu_model": cpu["cpu_model"],
+                            "sample": f"gids [0, {ccnt}) x numiter={4 * a.cpu_numiter} ({dta:.1f} s), one gid shard "
                                       f"per thread"}
 
     if D.rank == 0:
@@ -450,17 +564,15 @@ def run_ours(a, D):
             "metric": METRIC, "metric_detail": METRIC_DETAIL, "value": value, "unit": "numbers/s",
             "gbs": 8 * value / 1e9, "n_gpus": D.world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_max / a.steps, "higher_is_better": True,
-            "scaling": "strong" if a.numrn_total else "weak", "vs_baseline": None, "dtype": "u64",
+            "scaling": W["scaling"], "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (numrn, numiter, seed); outputs are the generated u64 stream",
-            "config": {"workload": (f"BASELINE config 2: numrn=2^{numrn.bit_length() - 1} ({numrn}) per iteration"
-                                    f" x numiter={a.numiter}, device-only" if D.world == 1 else
-                                    f"numrn={numrn} total ({cnt} per GPU, gid-range sharded) x numiter={a.numiter}"),
-                       "numrn": numrn, "numiter": a.numiter, "seed": a.seed, "parallelism": f"gid-shard{D.world}",
+            "config": {"workload": W["workload"], "numrn": numrn, "numiter": numiter, "per_gpu": cnt, "seed": a.seed,
+                       "parallelism": f"gid-shard{D.world}",
                        "output": ["state (paper)", "xorshift64* scrambled"][a.output],
                        "numa_bind": numa,
                        "l2": "output through a 64 GiB rotating ring per GPU (> 500x L2; no address rewritten "
                              "within 64 GiB, see profiles/r1_ring_absorption.md); no flush needed"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "sustained": sustained, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "probes": probes,
         }
         print(json.dumps(line), flush=True)

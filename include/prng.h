@@ -81,6 +81,11 @@ prng_t *prng_create(uint64_t numrn, uint64_t seed, prng_err_t *err);
 prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begin,
                           uint64_t gid_count, int cuda_device, prng_err_t *err);
 
+/* The handle's share of the stream: numrn_total, its first gid and its gid count (any
+ * pointer may be NULL).  PRNG_EINVAL for a NULL handle. */
+int prng_get_range(const prng_t *h, uint64_t *numrn_total, uint64_t *gid_begin, uint64_t *count,
+                   prng_err_t *err);
+
 /* NULL-safe.  Synchronises the handle's streams, frees device + pinned memory. */
 void prng_destroy(prng_t *h);
 
@@ -138,10 +143,11 @@ int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_
 int prng_device_ring(const prng_t *h, uint64_t **base, uint64_t *pitch, uint64_t *slots,
                      uint64_t *iter0_slot, uint64_t *last_iter_end, prng_err_t *err);
 
-/* Copy `count` outputs of device-ring slot `slot` to host memory (test/inspection aid). */
+/* Copy the handle's `count` outputs (prng_get_range) of device-ring slot `slot` to host
+ * memory, which must hold count u64 (test/inspection aid). */
 int prng_read_slot(prng_t *h, uint64_t slot, uint64_t *host_dst, prng_err_t *err);
 
-/* Copy the current per-gid state (== the last emitted iteration) to host memory. */
+/* Copy the current per-gid state (== the last emitted iteration; count u64) to host memory. */
 int prng_read_state(prng_t *h, uint64_t *host_dst, prng_err_t *err);
 
 /* ------------------------------------------------------------------ options */
@@ -162,14 +168,10 @@ enum prng_option {
                                   of 4; breaks power-of-two slot strides); default 0       */
     PRNG_OPT_HOST_MEM = 8,     /* pinned host halves of modes O1/O2/S0: 0 cudaHostAlloc,
                                   1 write-combined, 2 THP-backed mmap + cudaHostRegister  */
-    PRNG_OPT_TRACE_PTR = 9,    /* diagnostic: device pointer receiving %globaltimer stamps
-                                  [CTA][round][iteration / 64] from variant "v2n4s1t"      */
+                               /* 9: reserved (a round-1 diagnostic option, removed)        */
     PRNG_OPT_OUTPUT = 10,      /* NEXT-3 output transform: 0 = the state (the paper, A7);
                                   1 = state * 0x2545F4914F6CDD1D mod 2^64 (xorshift64*-style
-                                  scrambler, A19).  Needs a CTA-synchronised variant with
-                                  a scrambled instantiation ("auto", v4n4s1, v2n8s1,
-                                  v2n16s1, v4n8s1, v2n4s1, v4n16s1, v2n32s1, v4n8s1a,
-                                  v4n4s1a, v4n8s1p, v4n4s1p); others give PRNG_EINVAL.   */
+                                  scrambler, A19).  Every kernel variant supports both.    */
     PRNG_OPT_TIME_PARALLEL = 11, /* 1 (default): when numrn is too small to fill the GPU, cut
                                   a launch's iterations into chunks started by GF(2)
                                   jump-ahead (xs^k is linear: a 64x64 bit matrix); 0: off */
@@ -221,11 +223,12 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
  * PRNG_ESTATE otherwise).  best_gbs (may be NULL) gets the winner's probe GB/s. */
 int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err);
 
-/* Number of kernel variants compiled in, and the name of one (id 0 "auto", the default,
- * resolved per launch -- see PRNG_OPT_KERNEL; "v4n4s1" = one 32-byte store per thread per
- * iteration, 4 numbers per thread, CTA barrier every iteration; "v4n8s1" = the same with 8
- * numbers per thread; "v2n4s1" = two 16-byte stores; "v4n8" = 32-byte stores, 8 numbers
- * per thread, free-running warps).  NULL for an id out of range. */
+/* Number of kernel variants compiled in (8), and the name of one: id 0 "auto" (the
+ * default, resolved per launch -- see PRNG_OPT_KERNEL); "v<V>n<N>s1" = V-wide u64 vector
+ * stores (V = 4: 32 bytes, V = 2: 16 bytes), N numbers per thread, CTA barrier every
+ * iteration, 4 warps per SM; suffix "a" = .aligned barrier in uniform rounds, "p" =
+ * ping-pong hot loop.  "v2n4s1" is north_star's 16-byte form.  NULL for an id out of
+ * range. */
 int prng_kernel_variants(void);
 const char *prng_kernel_variant_name(int id);
 
@@ -293,23 +296,22 @@ int prng_prof_export(uint64_t nevents, const uint32_t *name_id, const double *st
                      const char *const *queues, const char *path, prng_err_t *err);
 
 /* ------------------------------------------------------------------ roofline probes */
-/* Same-box denominators: each returns GB/s (best of `reps`) or < 0 on
- * error.  bytes: buffer size. */
-double prng_probe_memset_gbs(uint64_t bytes, int reps);        /* cudaMemsetAsync write BW  */
+/* Same-box denominators, for bench.py: each returns GB/s or < 0 on
+ * error; `bytes` is the buffer size.  The store kernels write pseudo-random
+ * (incompressible) data, like the generator. */
+double prng_probe_memset_gbs(uint64_t bytes, int reps);  /* cudaMemsetAsync (copy engine), best of reps */
 /* The same fill repeated `reps` times back to back, timed as one interval (sustained,
  * power-capped write rate of the fill engine). */
 double prng_probe_memset_sustained_gbs(uint64_t bytes, int reps);
-double prng_probe_store_gbs(uint64_t bytes, int reps);         /* pure 32-B store kernel     */
-/* pattern 0 index, 1 zeros, 2 pseudo-random; warps_per_sm 0 = full occupancy */
-double prng_probe_store_pattern_gbs(uint64_t bytes, int reps, int pattern, int warps_per_sm);
-double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams); /* host link */
-double prng_probe_d2d_sweep_gbs(uint64_t chunk, uint64_t total, int reps); /* copy-engine sweep */
-/* research probe of SM store patterns (modes in prng_kernels.cuh store_pattern_kernel) */
-double prng_probe_store_mode_gbs(uint64_t bytes, int reps, int mode, int warps_per_cta, int ctas_per_sm,
-                                 uint64_t slots);
-/* research probe: SM store kernel and copy-engine D2D sweep concurrently (combined GB/s) */
-double prng_probe_concurrent_gbs(uint64_t sm_bytes, uint64_t ce_bytes, uint64_t ce_chunk, int sm_warps, int reps,
-                                 double *sm_alone, double *ce_alone);
+double prng_probe_store_gbs(uint64_t bytes, int reps);   /* persistent grid-stride 32-B store sweep */
+/* One-shot grid of 128-thread CTAs, each writing one contiguous 16 KiB chunk with 32-B
+ * stores (a framework fill kernel's structure): the fastest SM write pattern measured. */
+double prng_probe_fill_gbs(uint64_t bytes, int reps);
+/* Pinned (or pageable) cudaMemcpyAsync D2H over `nstreams` streams, best of `reps`. */
+double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams);
+/* `reps` pinned D2H copies back to back timed as one interval: each rank's sustained share
+ * of the host links when all ranks of a node run it at once (bench.py, N > 1). */
+double prng_probe_d2h_sustained_gbs(uint64_t bytes, int reps);
 
 #ifdef __cplusplus
 }

@@ -15,12 +15,13 @@ import numpy as np
 from ._build import LIB, build as _build_lib
 
 __all__ = [
-    "PrngError", "lib", "prng_create", "prng_create_range", "prng_destroy", "prng_init",
+    "PrngError", "lib", "prng_create", "prng_create_range", "prng_destroy", "prng_get_range", "prng_init",
     "prng_generate", "prng_generate_device", "prng_generate_host", "prng_seek", "prng_device_ring", "prng_read_slot",
     "prng_read_state", "prng_set_option", "prng_get_option", "prng_set_streams",
     "prng_strerror", "prng_prof_events", "prng_prof_calc", "prng_event_name",
     "prng_kernel_variants", "prng_kernel_variant_name", "prng_last_launch", "prng_autotune", "prng_probe_memset_gbs",
-    "prng_probe_store_gbs", "prng_probe_d2h_gbs", "SINK_NULL", "SINK_COPY", "SINK_DIGEST",
+    "prng_probe_store_gbs", "prng_probe_fill_gbs", "prng_probe_d2h_gbs",
+    "prng_probe_d2h_sustained_gbs", "SINK_NULL", "SINK_COPY", "SINK_DIGEST",
     "CopySink", "DigestSink", "SINK_FN",
     "PRNG_OPT_MODE", "PRNG_OPT_BATCH_ITERS", "PRNG_OPT_RING_SLOTS", "PRNG_OPT_PROFILE",
     "PRNG_OPT_KERNEL", "PRNG_OPT_GRID_WARPS", "PRNG_OPT_RING_PAD", "PRNG_OPT_HOST_MEM", "PRNG_OPT_CHUNK_ITERS",
@@ -32,7 +33,7 @@ __all__ = [
 PRNG_OK, PRNG_EINVAL, PRNG_ESTATE, PRNG_ENOMEM, PRNG_ECUDA, PRNG_ESINK = 0, -1, -2, -3, -4, -5
 PRNG_OPT_MODE, PRNG_OPT_BATCH_ITERS, PRNG_OPT_RING_SLOTS = 1, 2, 3
 PRNG_OPT_PROFILE, PRNG_OPT_KERNEL, PRNG_OPT_GRID_WARPS, PRNG_OPT_RING_PAD, PRNG_OPT_HOST_MEM = 4, 5, 6, 7, 8
-PRNG_OPT_TRACE_PTR, PRNG_OPT_OUTPUT, PRNG_OPT_TIME_PARALLEL, PRNG_OPT_BLOCKING, PRNG_OPT_CTA_WARPS = 9, 10, 11, 12, 13
+PRNG_OPT_OUTPUT, PRNG_OPT_TIME_PARALLEL, PRNG_OPT_BLOCKING, PRNG_OPT_CTA_WARPS = 10, 11, 12, 13
 PRNG_OPT_CHUNK_ITERS, PRNG_OPT_PIECE_ORDER, PRNG_OPT_EPOCH_ITERS = 14, 15, 16
 PRNG_MODE_SERIAL, PRNG_MODE_PAGEABLE, PRNG_MODE_OVERLAP1, PRNG_MODE_OVERLAP2, PRNG_MODE_ZEROCOPY = 0, 1, 2, 3, 4
 EV_NAMES = ("INIT_KERNEL", "RNG_KERNEL", "READ_BUFFER", "OUT")
@@ -53,7 +54,7 @@ class CopySink(ctypes.Structure):
 
 
 class DigestSink(ctypes.Structure):
-    _fields_ = [("xor_out", P64), ("sum_out", P64), ("iter_offset", u64), ("iters", u64)]
+    _fields_ = [("xor_out", P64), ("sum_out", P64), ("iter_offset", u64), ("iters", u64), ("wsum_out", P64)]
 
 
 SINK_FN = ctypes.CFUNCTYPE(ctypes.c_int, vp, u64, u32, u64, u64, P64)
@@ -84,6 +85,7 @@ def lib():
         "prng_create": ([u64, u64, E], vp),
         "prng_create_range": ([u64, u64, u64, u64, i32, E], vp),
         "prng_destroy": ([vp], None),
+        "prng_get_range": ([vp, P64, P64, P64, E], i32),
         "prng_set_streams": ([vp, vp, vp, E], i32),
         "prng_init": ([vp, E], i32),
         "prng_seek": ([vp, u64, E], i32),
@@ -107,11 +109,9 @@ def lib():
         "prng_probe_memset_gbs": ([u64, i32], dbl),
         "prng_probe_memset_sustained_gbs": ([u64, i32], dbl),
         "prng_probe_store_gbs": ([u64, i32], dbl),
-        "prng_probe_store_pattern_gbs": ([u64, i32, i32, i32], dbl),
+        "prng_probe_fill_gbs": ([u64, i32], dbl),
         "prng_probe_d2h_gbs": ([u64, i32, i32, i32], dbl),
-        "prng_probe_d2d_sweep_gbs": ([u64, u64, i32], dbl),
-        "prng_probe_store_mode_gbs": ([u64, i32, i32, i32, i32, u64], dbl),
-        "prng_probe_concurrent_gbs": ([u64, u64, u64, i32, i32, PD, PD], dbl),
+        "prng_probe_d2h_sustained_gbs": ([u64, i32], dbl),
         "prng_sink_null": ([vp, u64, u32, u64, u64, P64], i32),
         "prng_sink_copy": ([vp, u64, u32, u64, u64, P64], i32),
         "prng_sink_digest": ([vp, u64, u32, u64, u64, P64], i32),
@@ -169,6 +169,14 @@ def prng_destroy(h) -> None:
     lib().prng_destroy(h)
 
 
+def prng_get_range(h):
+    """-> (numrn_total, gid_begin, count) of the handle."""
+    err = prng_err_t()
+    n, b, c = u64(), u64(), u64()
+    _check(lib().prng_get_range(h, ctypes.byref(n), ctypes.byref(b), ctypes.byref(c), ctypes.byref(err)), err)
+    return n.value, b.value, c.value
+
+
 def prng_set_streams(h, gen_stream: int, copy_stream: int) -> None:
     err = prng_err_t()
     _check(lib().prng_set_streams(h, gen_stream, copy_stream, ctypes.byref(err)), err)
@@ -222,7 +230,15 @@ def prng_generate_device(h, numiter: int, dst_ptr: int, dst_pitch: int, dst_slot
 def prng_generate_host(h, numiter: int, dst: np.ndarray, dst_pitch: int, dst_rows: int, col_offset: int = 0) -> None:
     """D2H straight into a host array (shared-output multi-rank form): iteration k of the
     call -> dst.flat[(k % dst_rows) * dst_pitch + col_offset + j]."""
-    assert dst.dtype == np.uint64 and dst.flags["C_CONTIGUOUS"]
+    if dst.dtype != np.uint64 or not dst.flags["C_CONTIGUOUS"] or not dst.flags["WRITEABLE"]:
+        raise ValueError("dst must be a writeable C-contiguous uint64 array")
+    count = prng_get_range(h)[2]
+    if numiter >= 1 and dst_rows >= 1 and dst_pitch >= count:
+        # the span the DMA writes: rows 0 .. min(rows, numiter)-1, columns col_offset .. +count
+        need = (min(dst_rows, numiter) - 1) * dst_pitch + col_offset + count
+        if col_offset < 0 or col_offset + count > dst_pitch or dst.size < need:
+            raise ValueError(f"dst ({dst.size} u64) does not cover {need} u64 (rows {min(dst_rows, numiter)}, "
+                             f"pitch {dst_pitch}, col_offset {col_offset}, count {count})")
     err = prng_err_t()
     _check(lib().prng_generate_host(h, numiter, dst.ctypes.data + 8 * col_offset, dst_pitch, dst_rows,
                                     ctypes.byref(err)), err)
@@ -238,15 +254,21 @@ def prng_device_ring(h):
     return base.value, pitch.value, slots.value, first.value, end.value
 
 
-def prng_read_slot(h, slot: int, count: int) -> np.ndarray:
-    out = np.empty(count, dtype=np.uint64)
+def prng_read_slot(h, slot: int, count: int | None = None) -> np.ndarray:
+    n = prng_get_range(h)[2]
+    if count is not None and count != n:
+        raise ValueError(f"count {count} != the handle's count {n}")
+    out = np.empty(n, dtype=np.uint64)
     err = prng_err_t()
     _check(lib().prng_read_slot(h, slot, _ptr(out), ctypes.byref(err)), err)
     return out
 
 
-def prng_read_state(h, count: int) -> np.ndarray:
-    out = np.empty(count, dtype=np.uint64)
+def prng_read_state(h, count: int | None = None) -> np.ndarray:
+    n = prng_get_range(h)[2]
+    if count is not None and count != n:
+        raise ValueError(f"count {count} != the handle's count {n}")
+    out = np.empty(n, dtype=np.uint64)
     err = prng_err_t()
     _check(lib().prng_read_state(h, _ptr(out), ctypes.byref(err)), err)
     return out
@@ -379,13 +401,13 @@ def prng_probe_store_gbs(nbytes: int, reps: int = 5) -> float:
     return lib().prng_probe_store_gbs(nbytes, reps)
 
 
-def prng_probe_d2d_sweep_gbs(chunk: int, total: int, reps: int = 3) -> float:
-    return lib().prng_probe_d2d_sweep_gbs(chunk, total, reps)
-
-
-def prng_probe_store_pattern_gbs(nbytes: int, reps: int = 3, pattern: int = 0, warps_per_sm: int = 0) -> float:
-    return lib().prng_probe_store_pattern_gbs(nbytes, reps, pattern, warps_per_sm)
+def prng_probe_fill_gbs(nbytes: int, reps: int = 5) -> float:
+    return lib().prng_probe_fill_gbs(nbytes, reps)
 
 
 def prng_probe_d2h_gbs(nbytes: int, reps: int = 5, pinned: bool = True, nstreams: int = 1) -> float:
     return lib().prng_probe_d2h_gbs(nbytes, reps, int(pinned), nstreams)
+
+
+def prng_probe_d2h_sustained_gbs(nbytes: int, reps: int = 8) -> float:
+    return lib().prng_probe_d2h_sustained_gbs(nbytes, reps)

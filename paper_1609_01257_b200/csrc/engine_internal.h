@@ -44,7 +44,7 @@ inline int ok(prng_err_t *err) {
     } while (0)
 
 constexpr int kBlock = 256;     // threads per CTA of the batch kernels (max)
-constexpr int kMaxVariants = 64;
+constexpr int kMaxVariants = 16;
 
 inline double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -100,9 +100,12 @@ struct prng {
     int64_t epoch_iters = 0;  // PRNG_OPT_EPOCH_ITERS
     int last_kernel = -1;     // variant id of the last batch launch (after the anti-absorption rule)
     uint32_t last_epoch = 0;  // its epoch length (0: natural order)
-    unsigned long long *trace = nullptr;  // PRNG_OPT_TRACE_PTR (diagnostic variant only)
 
     int profile = 0, kernel = 0, output = 0, blocking = 1;
+    // Test-only fault injection (env PRNG_B200_FAULT_AFTER=N, read at create): the N-th
+    // checked CUDA call of prng_generate_host reports failure, so tests can prove that a
+    // failed record / wait / copy poisons the handle instead of returning silent output.
+    int64_t fault_after = 0;
     int blocks_per_sm[prng_detail::kMaxVariants] = {0};
 
     // profiling (a6)
@@ -122,6 +125,11 @@ struct prng {
 };
 
 namespace prng_detail {
+
+inline cudaError_t fault_point(prng *h, cudaError_t e) {
+    if (e == cudaSuccess && h->fault_after > 0 && --h->fault_after == 0) return cudaErrorUnknown;
+    return e;
+}
 
 void free_host(int kind, void *p, size_t bytes);
 void free_e2e(prng *h);

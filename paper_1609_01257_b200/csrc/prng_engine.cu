@@ -30,115 +30,50 @@ using namespace prng_detail;
 namespace {
 
 // ============================================================================ kernel variants
+// Every variant: one warp owns a piece of 32 x NPT consecutive gids (VEC-wide vector stores,
+// NPT numbers per thread), 4 warps per SM in one CTA, the CTA's warps meet at a barrier
+// every iteration (so a CTA writes one contiguous chunk per iteration).  Each carries its
+// scrambled-output (NEXT-3) and epoch-order (anti-absorption) instantiations.
+// Round 1 measured ~40 more forms (free-running warps, cluster barriers, cache policies,
+// barrier intervals, TMA bulk stores, interleaved vectors, a lean single-path loop); none
+// was faster at the bench shape, and they were removed from the library in round 2
+// (results: profiles/r1_sweeps.md, profiles/r1_l2_absorption.md; code: git history before
+// the "strip experiment variants" commit).
 using BatchFn = void (*)(prngk::BatchArgs);
 struct Variant {
     const char *name;
-    int vec, npt, policy, sync, cluster;  // sync: 0 none, 1 CTA barrier, 2 cluster barrier
-    int warps_per_sm;                     // default grid: resident warps per SM (0 = occupancy max)
-    BatchFn fn;
-    int stages;                           // > 0: TMA bulk-store kernel with this many smem stages
-    BatchFn star;                         // NEXT-3 xorshift64* output instantiation (nullptr: none)
-    BatchFn epoch, epoch_star;            // epoch-major instantiations (nullptr: none)
-    BatchFn lean = nullptr, lean_star = nullptr;  // single-path form for launches whose pieces
-                                                  // are all full, natural order (nullptr: none)
+    int vec, npt;                  // vector width (u64) and numbers per thread
+    int warps_per_sm;              // default grid: resident warps per SM
+    BatchFn fn, star;              // natural order: state output / xorshift64* output (NEXT-3)
+    BatchFn epoch, epoch_star;     // epoch-major order (anti-absorption)
 };
-#define V(name, vec, npt, pol, sync, cl, wps) \
-    {name, vec, npt, pol, sync, cl, wps, prngk::batch_kernel<vec, npt, pol, sync>, 0, nullptr, nullptr, nullptr}
-// CTA-synchronised variants that also carry the NEXT-3 scrambled-output and the
-// epoch-major instantiations
-#define VS(name, vec, npt, wps) VSA(name, vec, npt, wps, false)
-// ... with the ping-pong hot loop (PP, prngk::run_piece)
-#define VSP(name, vec, npt, wps, al)                                                                      \
-    {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1, 0, al, false, true>, 0,             \
-     prngk::batch_kernel<vec, npt, 0, 1, 1, al, false, true>, prngk::batch_kernel_epoch<vec, npt, 0, al>, \
-     prngk::batch_kernel_epoch<vec, npt, 1, al>}
-// ... with the .aligned CTA barrier in uniform rounds (AL, prngk::cta_barrier)
-#define VSA(name, vec, npt, wps, al)                                                                 \
-    {name, vec, npt, 0, 1, 1, wps, prngk::batch_kernel<vec, npt, 0, 1, 0, al>, 0,                   \
-     prngk::batch_kernel<vec, npt, 0, 1, 1, al>, prngk::batch_kernel_epoch<vec, npt, 0, al>,       \
-     prngk::batch_kernel_epoch<vec, npt, 1, al>}
-#define VT(name, npt, stages, wps) \
-    {name, 2, npt, 0, 0, 1, wps, prngk::batch_kernel_tma<npt, stages>, stages, nullptr, nullptr, nullptr}
-// CTA-coherent TMA stores (one cp.async.bulk of the CTA's whole chunk per iteration)
-#define VTC(name, npt, stages, pw) \
-    {name, 4, npt, 0, 1, 1, 4, prngk::batch_kernel_tmac<npt, stages, pw>, stages, nullptr, nullptr, nullptr}
+// AL: .aligned CTA barrier in uniform rounds; PP: ping-pong hot loop (prngk::run_piece)
+#define VAR(name, vec, npt, al, pp)                                                             \
+    {name, vec, npt, 4, prngk::batch_kernel<vec, npt, 0, al, pp>, prngk::batch_kernel<vec, npt, 1, al, pp>, \
+     prngk::batch_kernel_epoch<vec, npt, 0, al>, prngk::batch_kernel_epoch<vec, npt, 1, al>}
 // Measured on B200 at numrn = 2^24 x 1000 through a non-reused 64 GiB ring
-// (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 16-/32-B vectors reach
-// 6.6-6.8 TB/s (~90 % of the same-box cudaMemset fill rate; one 32-B store per thread is
-// ~2 % ahead of two 16-B ones, 7.29 TB/s at numrn = 2^27); free-running warps at full
-// occupancy ~6.2 TB/s (more concurrently open DRAM pages).
+// (profiles/r1_sweeps.md): 4 CTA-synchronised warps per SM writing 32-B vectors reach
+// 6.6-6.9 TB/s with DRAM bytes = algorithmic bytes.
 const Variant kVariants[] = {
     // id 0 "auto" (the default): resolved per launch by launch_batch -- v4n8s1a at >= 2^21
     // work-items per handle, v4n4s1p below (measured), then widened or run in
     // epoch order by the anti-absorption rule.  Its own fields (= v4n4s1) size the grid.
-    VS("auto", 4, 4, 4),
-    VS("v2n8s1", 2, 8, 4),  VS("v2n16s1", 2, 16, 4), VS("v4n8s1", 4, 8, 4),
-    // free-running warps
-    V("v4n8", 4, 8, 0, 0, 1, 0),      V("v2n4", 2, 4, 0, 0, 1, 0),     V("v2n8", 2, 8, 0, 0, 1, 0),
-    V("v4n4", 4, 4, 0, 0, 1, 0),      V("v4n16", 4, 16, 0, 0, 1, 0),   V("v2n16", 2, 16, 0, 0, 1, 0),
-    V("v4n8cs", 4, 8, 1, 0, 1, 0),    V("v2n8cs", 2, 8, 1, 0, 1, 0),
-    // cluster barrier (split arrive / wait) every iteration (c2 ~ s1; c4 ~ 4.4 TB/s)
-    V("v2n8c2", 2, 8, 0, 2, 2, 4),    V("v2n8c4", 2, 8, 0, 2, 4, 4),
-    // the bench geometry (32-B stores, 8 numbers per thread) with a 2-CTA cluster barrier
-    V("v4n8c2", 4, 8, 0, 2, 2, 4),
-    // v4n8s1a with store cache policies: .cs, L2::evict_first hint, L1::no_allocate
-    {"v4n8s1a_cs", 4, 8, 1, 1, 1, 4, prngk::batch_kernel<4, 8, 1, 1, 0, true>, 0, nullptr, nullptr, nullptr},
-    {"v4n8s1a_ef", 4, 8, 2, 1, 1, 4, prngk::batch_kernel<4, 8, 2, 1, 0, true>, 0, nullptr, nullptr, nullptr},
-    {"v4n8s1a_na", 4, 8, 3, 1, 1, 4, prngk::batch_kernel<4, 8, 3, 1, 0, true>, 0, nullptr, nullptr, nullptr},
-    // long per-CTA chunks: 32 / 64 numbers per thread (16 / 32 KiB per warp per iteration)
-    // (measured: no gain over v2n4s1; 64 numbers/thread spills and was removed)
-    VS("v2n32s1", 2, 32, 4),  V("v4n32s1", 4, 32, 0, 1, 1, 4),
-    // fewer instructions per number (32-B stores, more numbers per thread): less SM power
-    V("v4n12s1", 4, 12, 0, 1, 1, 4),  VS("v4n16s1", 4, 16, 4),
-    // store cache policies on the default structure: .cs, L2::evict_first, L1::no_allocate
-    V("v2n4s1cs", 2, 4, 1, 1, 1, 4),  V("v2n4s1ef", 2, 4, 2, 1, 1, 4), V("v2n4s1na", 2, 4, 3, 1, 1, 4),
-    // diagnostic: v2n4s1 + per-CTA %globaltimer trace (PRNG_OPT_TRACE_PTR)
-    V("v2n4s1t", 2, 4, 0, 3, 1, 4),
-    // TMA bulk stores: one cp.async.bulk per warp per iteration from an smem stage ring
-    VT("t2n4", 4, 4, 4),   VT("t2n8", 8, 4, 4),   VT("t2n16", 16, 4, 4),  VT("t2n8s8", 8, 8, 4),
-    VT("t2n4w8", 4, 4, 8), VT("t2n8w8", 8, 4, 8),
-    // the round-1 default: two 16-B stores per thread per iteration (r1_sweeps.md "32-B stores")
-    VS("v2n4s1", 2, 4, 4),
-    // one 32-B store per thread per iteration, 4 numbers/thread, CTA barrier, 4 warps/SM:
-    // the default until session 2 of round 1 (now "auto" below 2^21 work-items)
-    VS("v4n4s1", 4, 4, 4),
-    // CTA barrier form (exp29): the .aligned bar.sync in uniform rounds, non-.aligned
-    // barrier.sync otherwise -- v4n8s1 2.3 % faster with it at the bench shape, v4n4s1
-    // 5 % slower; "auto" uses v4n8s1a
-    VSA("v4n8s1a", 4, 8, 4, true),   VSA("v4n4s1a", 4, 4, 4, true),
-    // CTA barrier every 2 / 4 iterations (experiment, .aligned in uniform rounds)
-    {"v4n8s2a", 4, 8, 0, 5, 1, 4, prngk::batch_kernel<4, 8, 0, 5, 0, true>, 0, nullptr, nullptr, nullptr},
-    {"v4n8s4a", 4, 8, 0, 6, 1, 4, prngk::batch_kernel<4, 8, 0, 6, 0, true>, 0, nullptr, nullptr, nullptr},
-    // CTA-coherent TMA bulk stores: the v4n8s1a structure, one 8 KiB bulk copy per CTA per
-    // iteration from a ring of S = 3 / 4 shared-memory stages
-    // ping-pong hot loop: no register copies before the 32-B stores
-    VSP("v4n8s1p", 4, 8, 4, true), VSP("v4n4s1p", 4, 4, 4, false),
-    // the same with the lean single-path kernel when every piece is full (batch_kernel_lean)
-    {"v4n8s1l", 4, 8, 0, 1, 1, 4, prngk::batch_kernel<4, 8, 0, 1, 0, true, false, true>, 0,
-     prngk::batch_kernel<4, 8, 0, 1, 1, true, false, true>, prngk::batch_kernel_epoch<4, 8, 0, true>,
-     prngk::batch_kernel_epoch<4, 8, 1, true>, prngk::batch_kernel_lean<4, 8, 0>, prngk::batch_kernel_lean<4, 8, 1>},
-    {"v4n4s1l", 4, 4, 0, 1, 1, 4, prngk::batch_kernel<4, 4, 0, 1, 0, false, false, true>, 0,
-     prngk::batch_kernel<4, 4, 0, 1, 1, false, false, true>, prngk::batch_kernel_epoch<4, 4, 0, false>,
-     prngk::batch_kernel_epoch<4, 4, 1, false>, prngk::batch_kernel_lean<4, 4, 0>, prngk::batch_kernel_lean<4, 4, 1>},
-    VSP("v4n16s1p", 4, 16, 4, true), VSP("v2n32s1p", 2, 32, 4, true),
-    // v4n8s1a with the CTA's warps interleaving their vectors over the CTA's chunk
-    {"v4n8s1ai", 4, 8, 0, 1, 1, 4, prngk::batch_kernel<4, 8, 0, 1, 0, true, true>, 0, nullptr, nullptr, nullptr},
-    VTC("c4n8s3", 8, 3, false), VTC("c4n8s4", 8, 4, false), VTC("c4n8s8", 8, 8, false),
-    VTC("c4n8s16", 8, 16, false),
-    // ... one bulk copy per warp (its own 2 KiB piece) after the CTA barrier
-    VTC("w4n8s4", 8, 4, true), VTC("w4n8s8", 8, 8, true),
+    VAR("auto", 4, 4, false, false),
+    // the bench-shape default: one 32-B store per thread per vector, 8 numbers per thread
+    // (2 KiB per warp-iteration), .aligned barrier in uniform rounds
+    VAR("v4n8s1a", 4, 8, true, false),
+    // the default below 2^21 work-items: 4 numbers per thread, ping-pong hot loop
+    VAR("v4n4s1p", 4, 4, false, true),
+    // the anti-absorption substitutes, 2 / 4 / 8 KiB per warp-iteration
+    VAR("v4n8s1", 4, 8, false, false), VAR("v4n16s1", 4, 16, false, false), VAR("v2n32s1", 2, 32, false, false),
+    // north_star's 16-byte form: two st.global.v2.u64 per thread per iteration (the round-1
+    // default; bit-identical output, 1.5-3 % slower than the 32-B forms on B200)
+    VAR("v2n4s1", 2, 4, false, false),
+    // one 32-B store per thread, 4 numbers per thread (the round-1 default after v2n4s1)
+    VAR("v4n4s1", 4, 4, false, false),
 };
-#undef VTC
-#undef VT
-#undef VSP
-#undef VSA
-#undef VS
-#undef V
+#undef VAR
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
-
-size_t variant_smem(const Variant &v, uint64_t warps_per_block) {
-    return v.stages ? (size_t)warps_per_block * v.stages * 32 * v.npt * sizeof(uint64_t) : 0;
-}
 static_assert(kNumVariants <= kMaxVariants, "raise kMaxVariants");
 
 }  // namespace
@@ -296,12 +231,8 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
             }
         }
     }
-    const Variant &v0 = kVariants[vid];
-    Variant v = v0;
-    if (h->output == 1) {
-        if (!v0.star) return set_err(err, PRNG_EINVAL, "output scrambling not compiled for variant %s", v0.name);
-        v.fn = v0.star;
-    }
+    const Variant &v = kVariants[vid];
+    BatchFn fn = h->output == 1 ? v.star : v.fn;
     prngk::BatchArgs a;
     a.dst = dst;
     a.pitch = pitch;
@@ -311,12 +242,11 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     a.count = h->count;
     a.iters = iters;
     a.first_is_state = first_is_state ? 1u : 0u;
-    a.trace = h->trace;
     a.nchunks = 1;
     a.chunk_len = iters;
     a.jump = nullptr;
     a.state_out = h->d_state;
-    a.order = (v.stages == 0 && v.cluster <= 1) ? (uint32_t)h->piece_order : 0u;
+    a.order = (uint32_t)h->piece_order;
 
     const uint64_t piece = 32ull * v.npt;
     a.npieces = (h->count + piece - 1) / piece;
@@ -332,27 +262,23 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // write the same slot and the earlier iteration could land last.
     uint64_t nch = 0;
     if (iters <= nslots) {
-        if (v.stages == 0 && h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters)
+        if (h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters)
             nch = (iters + h->chunk_iters - 1) / h->chunk_iters;  // PRNG_OPT_CHUNK_ITERS: forced
-        else if (h->time_parallel && v.stages == 0 && 2 * a.npieces <= max_warps && iters >= 512)
+        else if (h->time_parallel && 2 * a.npieces <= max_warps && iters >= 512)
             nch = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
     }
     // Anti-absorption, fallback: epoch-major order (batch_kernel_epoch) with E = R, so an
     // address is rewritten only one whole epoch (the full ring) later.
     uint64_t E = 0;
-    if (v.epoch && nch <= 1 && h->epoch_iters >= 0) {
+    if (nch <= 1 && h->epoch_iters >= 0) {
         if (h->epoch_iters > 0)
             E = (uint64_t)h->epoch_iters;  // PRNG_OPT_EPOCH_ITERS: forced
         else if (absorbs(h, vid, nslots, iters, wps))
             E = nslots;
         if (E >= iters) E = 0;
     }
-    // lean single-path kernel: every piece full, natural order, no chunks, default grid
-    // shape (one CTA of <= 8 warps per SM or 256-thread CTAs, as for the regular kernel)
-    if (v0.lean && E == 0 && nch <= 1 && a.order == 0 && h->count % piece == 0)
-        v.fn = h->output == 1 ? v0.lean_star : v0.lean;
     if (E > 0) {
-        v.fn = h->output == 1 ? v0.epoch_star : v0.epoch;
+        fn = h->output == 1 ? v.epoch_star : v.epoch;
         a.nchunks = (uint32_t)((iters + E - 1) / E);
         a.chunk_len = (uint32_t)E;
     } else if (nch > 1) {
@@ -388,44 +314,13 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // ceil(warps / SMs) warps, else 256-thread CTAs.
     uint64_t wpb = kBlock / 32;
     if (warps <= (uint64_t)h->num_sms * wpb) wpb = std::max<uint64_t>(1, (warps + h->num_sms - 1) / h->num_sms);
-    if (h->cta_warps > 0 && v.stages == 0) wpb = (uint64_t)h->cta_warps;  // PRNG_OPT_CTA_WARPS
+    if (h->cta_warps > 0) wpb = (uint64_t)h->cta_warps;  // PRNG_OPT_CTA_WARPS
     uint64_t blocks = (warps + wpb - 1) / wpb;
-    const uint64_t C = (uint64_t)v.cluster;
-    if (C > 1) {
-        // whole clusters only, and no more clusters than can be co-resident
-        int max_cl = 0;
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)C;
-        at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3((unsigned)(((blocks + C - 1) / C) * C));
-        cfg.blockDim = dim3((unsigned)(32 * wpb));
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CU(cudaOccupancyMaxActiveClusters(&max_cl, v.fn, &cfg));
-        if (max_cl < 1) return set_err(err, PRNG_ECUDA, "cluster of %llu CTAs cannot be resident", (unsigned long long)C);
-        blocks = std::min<uint64_t>((blocks + C - 1) / C, (uint64_t)max_cl) * C;
-    }
     a.rounds = (uint32_t)((units + blocks * wpb - 1) / (blocks * wpb));
     h->last_kernel = vid;
     h->last_epoch = (uint32_t)E;
     if (int rc = prof_begin(h, s, PRNG_EV_RNG_KERNEL, err)) return rc;
-    if (C > 1) {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)C;
-        at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3((unsigned)blocks);
-        cfg.blockDim = dim3((unsigned)(32 * wpb));
-        cfg.stream = s;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CU(cudaLaunchKernelEx(&cfg, v.fn, a));
-    } else {
-        v.fn<<<(unsigned)blocks, (unsigned)(32 * wpb), variant_smem(v, wpb), s>>>(a);
-    }
+    fn<<<(unsigned)blocks, (unsigned)(32 * wpb), 0, s>>>(a);
     if (a.jump) std::swap(h->d_state, h->d_state2);  // time-parallel: the final state is in the other half
     CU(cudaGetLastError());
     return prof_end(h, s, err);
@@ -505,6 +400,7 @@ prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begi
         return nullptr;
     }
     h->device = dev;
+    if (const char *f = std::getenv("PRNG_B200_FAULT_AFTER")) h->fault_after = std::atoll(f);
     h->numrn_total = numrn_total;
     h->seed = seed;
     h->gid_begin = gid_begin;
@@ -518,17 +414,8 @@ prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begi
     if ((e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
         return bail("cudaDeviceGetAttribute(SMs)", e);
     cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, dev);
-    int smem_optin = 48 * 1024;
-    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     for (int i = 0; i < kNumVariants; ++i) {
-        // stage kernels size their shared memory per launch (warps per CTA x stages); allow
-        // up to the opt-in maximum, and size occupancy for the largest CTA that fits
-        const size_t smem = std::min<size_t>(variant_smem(kVariants[i], kBlock / 32), (size_t)smem_optin);
-        if (smem > 48 * 1024 &&
-            (e = cudaFuncSetAttribute(kVariants[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-                cudaSuccess)
-            return bail("cudaFuncSetAttribute(smem)", e);
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm[i], kVariants[i].fn, kBlock, smem)) !=
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm[i], kVariants[i].fn, kBlock, 0)) !=
             cudaSuccess)
             return bail("cudaOccupancyMaxActiveBlocksPerMultiprocessor", e);
         if (h->blocks_per_sm[i] < 1) h->blocks_per_sm[i] = 1;
@@ -541,6 +428,14 @@ prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begi
         return bail("cudaStreamCreate", e);
     ok(err);
     return h;
+}
+
+int prng_get_range(const prng_t *h, uint64_t *numrn_total, uint64_t *gid_begin, uint64_t *count, prng_err_t *err) {
+    if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
+    if (numrn_total) *numrn_total = h->numrn_total;
+    if (gid_begin) *gid_begin = h->gid_begin;
+    if (count) *count = h->count;
+    return ok(err);
 }
 
 prng_t *prng_create(uint64_t numrn, uint64_t seed, prng_err_t *err) {
@@ -567,6 +462,9 @@ void prng_destroy(prng_t *h) {
 
 int prng_set_streams(prng_t *h, void *gen_stream, void *copy_stream, prng_err_t *err) {
     if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
+    // validate before touching the handle: a rejected call leaves its streams as they were
+    if (!gen_stream || !copy_stream || gen_stream == copy_stream)
+        return set_err(err, PRNG_EINVAL, "need two distinct non-NULL streams");
     CU(cudaSetDevice(h->device));
     CU(cudaStreamSynchronize(h->s_gen));
     CU(cudaStreamSynchronize(h->s_copy));
@@ -577,8 +475,6 @@ int prng_set_streams(prng_t *h, void *gen_stream, void *copy_stream, prng_err_t 
     h->s_gen = (cudaStream_t)gen_stream;
     h->s_copy = (cudaStream_t)copy_stream;
     h->own_streams = false;
-    if (!h->s_gen || !h->s_copy || h->s_gen == h->s_copy)
-        return set_err(err, PRNG_EINVAL, "need two distinct non-NULL streams");
     return ok(err);
 }
 
@@ -621,8 +517,6 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             break;
         case PRNG_OPT_KERNEL:
             if (value < 0 || value >= kNumVariants) return set_err(err, PRNG_EINVAL, "bad kernel variant");
-            if (h->output == 1 && !kVariants[value].star)
-                return set_err(err, PRNG_EINVAL, "output scrambling not compiled for variant %s", kVariants[value].name);
             h->kernel = (int)value;
             break;
         case PRNG_OPT_TIME_PARALLEL:
@@ -634,8 +528,6 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             break;
         case PRNG_OPT_OUTPUT:
             if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad output transform");
-            if (value == 1 && !kVariants[h->kernel].star)
-                return set_err(err, PRNG_EINVAL, "output scrambling not compiled for variant %s", kVariants[h->kernel].name);
             h->output = (int)value;
             break;
         case PRNG_OPT_GRID_WARPS:
@@ -649,9 +541,6 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
         case PRNG_OPT_HOST_MEM:
             if (value < HK_PINNED || value > HK_HUGE_REGISTERED) return set_err(err, PRNG_EINVAL, "bad host mem kind");
             h->host_mem = (int)value;
-            break;
-        case PRNG_OPT_TRACE_PTR:
-            h->trace = (unsigned long long *)(uintptr_t)value;
             break;
         case PRNG_OPT_CHUNK_ITERS:
             if (value < 0 || value > 0xFFFFFFFFll) return set_err(err, PRNG_EINVAL, "bad chunk iterations");
@@ -688,7 +577,6 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_GRID_WARPS: *value = h->grid_warps; break;
         case PRNG_OPT_RING_PAD: *value = h->ring_pad; break;
         case PRNG_OPT_HOST_MEM: *value = h->host_mem; break;
-        case PRNG_OPT_TRACE_PTR: *value = (int64_t)(uintptr_t)h->trace; break;
         case PRNG_OPT_CHUNK_ITERS: *value = h->chunk_iters; break;
         case PRNG_OPT_PIECE_ORDER: *value = h->piece_order; break;
         case PRNG_OPT_EPOCH_ITERS: *value = h->epoch_iters; break;
@@ -852,8 +740,8 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
 static const struct {
     const char *variant;
     int warps_per_sm;
-} kTuneCandidates[] = {{"v4n4s1p", 4}, {"v2n4s1", 4}, {"v2n4s1", 8}, {"v2n8s1", 4},
-                       {"v2n16s1", 4}, {"v2n8c2", 4}, {"v4n8s1a", 4}, {"t2n8w8", 8}};
+} kTuneCandidates[] = {{"v4n8s1a", 4}, {"v4n4s1p", 4}, {"v4n4s1", 4}, {"v2n4s1", 4},
+                       {"v2n4s1", 8},  {"v4n8s1", 4},  {"v4n16s1", 4}, {"v2n32s1", 8}};
 
 extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err) {
     if (int rc = check_handle(h, err, false)) return rc;
@@ -873,9 +761,7 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
     int64_t best_w = h->grid_warps;
     int rc = PRNG_OK;
     for (const auto &c : kTuneCandidates) {
-        int k = -1;
-        for (int i = 0; i < kNumVariants; ++i)
-            if (!std::strcmp(kVariants[i].name, c.variant)) k = i;
+        const int k = variant_id(c.variant);
         if (k < 0) continue;
         h->kernel = k;
         h->grid_warps = (int64_t)c.warps_per_sm * h->num_sms;

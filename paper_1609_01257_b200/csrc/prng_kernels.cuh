@@ -77,36 +77,13 @@ __device__ __forceinline__ uint64_t emit(uint64_t x) {
 }
 
 // ---------------------------------------------------------------- vector memory helpers
-// POLICY 0: default write-back; 1: .cs (streaming, evict-first) -- the output is never
-// re-read by the SMs, only by the copy engine.
-// POLICY 2: L2 evict_first cache-hint policy; 3: L1::no_allocate.
-template <int POLICY>
+// Plain write-back stores: the measured alternatives (.cs, L2::evict_first, L1::no_allocate,
+// TMA bulk stores from shared memory) were not faster on B200.
 __device__ __forceinline__ void st_v4(uint64_t *p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
-    if constexpr (POLICY == 1)
-        asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
-    else if constexpr (POLICY == 2)
-        asm volatile(
-            "{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-            "st.global.L2::cache_hint.v4.u64 [%0], {%1, %2, %3, %4}, pol; }" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d)
-            : "memory");
-    else if constexpr (POLICY == 3)
-        asm volatile("st.global.L1::no_allocate.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
-                     "l"(d) : "memory");
-    else
-        asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
 }
-template <int POLICY>
 __device__ __forceinline__ void st_v2(uint64_t *p, uint64_t a, uint64_t b) {
-    if constexpr (POLICY == 1)
-        asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
-    else if constexpr (POLICY == 2)
-        asm volatile(
-            "{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-            "st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, pol; }" ::"l"(p), "l"(a), "l"(b) : "memory");
-    else if constexpr (POLICY == 3)
-        asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
-    else
-        asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 __device__ __forceinline__ void ld_v4(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
     asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
@@ -115,12 +92,12 @@ __device__ __forceinline__ void ld_v2(const uint64_t *p, uint64_t &a, uint64_t &
     asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
 }
 
-template <int VEC, int POLICY>
+template <int VEC>
 __device__ __forceinline__ void store_vec(uint64_t *p, const uint64_t *x) {
     if constexpr (VEC == 4)
-        st_v4<POLICY>(p, x[0], x[1], x[2], x[3]);
+        st_v4(p, x[0], x[1], x[2], x[3]);
     else
-        st_v2<POLICY>(p, x[0], x[1]);
+        st_v2(p, x[0], x[1]);
 }
 template <int VEC>
 __device__ __forceinline__ void load_vec(const uint64_t *p, uint64_t *x) {
@@ -149,7 +126,7 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
         const uint64_t s0 = seed64(g, key_hi, key_lo);
         if (i + 1 < a.count) {
             const uint64_t s1 = seed64(g + 1u, key_hi, key_lo);
-            st_v2<0>(a.state + i, s0, s1);
+            st_v2(a.state + i, s0, s1);
         } else {
             a.state[i] = s0;
         }
@@ -169,11 +146,11 @@ struct BatchArgs {
                               //    emit the state unchanged, then step (A6)
     uint64_t npieces;         // ceil(count / (32 * NPT))
     uint32_t rounds;          // ceil(npieces * nchunks / warps in grid)
-    unsigned long long *trace;  // SYNC 3 (diagnostic): %globaltimer per CTA, round, 64 iterations
     // Time-parallel mode (NEXT-4, small numrn): the launch's iterations are cut into nchunks
     // chunks of chunk_len; chunk c starts from J_c * state where J_c = T^(c*chunk_len + e)
     // is the GF(2) matrix of xs^(c*chunk_len + e) (e = 0 if first_is_state else 1), stored
     // as 64 columns J_c e_i at jump[c*64 + i].  nchunks == 1: the plain sequential mode.
+    // The epoch kernel reuses nchunks / chunk_len as its epoch count / length.
     uint32_t nchunks;
     uint32_t chunk_len;
     const uint64_t *jump;     // [nchunks][64] (nchunks > 1)
@@ -250,27 +227,16 @@ struct Unit {
     bool emit_first;       // true: the unit's first iteration emits its start value unchanged
 };
 
-// Warp coherence (SYNC):
-//   0  none: every warp runs its piece at its own pace.
-//   1  CTA:  the warps of a CTA (adjacent pieces) meet at a named barrier every iteration,
-//            so a CTA writes one contiguous chunk per iteration.
-//   2  cluster: the CTAs of a thread-block cluster (adjacent pieces again) meet at a
-//            split hardware cluster barrier every iteration: arrive right after the
-//            iteration's stores are issued, wait just before the next iteration's stores,
-//            so the xorshift arithmetic overlaps the barrier.  Warps without a piece in
-//            the last round still take part in the barriers (IDLE mode).
-//   5, 6  as 1, but the barrier only every 2 / 4 iterations (experiment)
-//   3  as 1, plus a %globaltimer trace (diagnostic: measured CTA drift of ~180 iterations
-//            at numrn = 2^24, i.e. the grid writes ~180 ring slots at once).
-// Fewer drifting write streams -> fewer concurrently open DRAM pages.
-enum PieceMode { FULL = 0, PARTIAL = 1, IDLE = 2 };
+enum PieceMode { FULL = 0, PARTIAL = 1 };
 
-// The per-iteration CTA barrier (named barrier 1 over the CTA's active warps).  The
-// non-.aligned form: the warps of one CTA reach it from different instructions (full and
-// partial pieces, the peeled first trip, idle trips), which `bar.sync` (= barrier.sync
-// .aligned) does not allow -- compute-sanitizer synccheck flags it.
-// AL = true: the CTA's warps are known to run identical instruction sequences this round
-// (all full pieces, same trip count), which is what the .aligned `bar.sync` requires.
+// The per-iteration CTA barrier: the warps of a CTA (adjacent pieces) meet at named barrier
+// 1 after every iteration's stores, so a CTA writes one contiguous chunk per iteration
+// (measured: -6 % without it; free-running warps at full occupancy ~6.2 TB/s against
+// 6.7-6.9).  The non-.aligned form by default: the warps of one CTA reach it
+// from different instructions (full and partial pieces, the peeled first trip, idle trips),
+// which `bar.sync` (= barrier.sync.aligned) does not allow -- compute-sanitizer synccheck
+// flags it.  AL = true: the CTA's warps are known to run identical instruction sequences
+// this round (all full pieces, same trip count), which the .aligned form needs.
 template <bool AL = false>
 __device__ __forceinline__ void cta_barrier(uint32_t threads) {
     if constexpr (AL)
@@ -279,100 +245,63 @@ __device__ __forceinline__ void cta_barrier(uint32_t threads) {
         asm volatile("barrier.sync 1, %0;" ::"r"(threads) : "memory");
 }
 
-__device__ __forceinline__ void cluster_arrive() {
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
-
-// IL (full pieces only): the lane's NPT / VEC vectors are `ilstride` elements apart instead
-// of 32 x VEC -- the CTA's warps interleave their vectors over the CTA's contiguous chunk
-// (u.base set accordingly by the caller), so each store instruction wave of the CTA covers
-// one contiguous wpb x 32 x VEC x 8 B run.
 // PP: the hot loop is unrolled by two with the state ping-ponging between two register
 // arrays, so each step's results land directly in the registers the next 32-B store
 // reads (without it ptxas copies 8 registers into a staging octet before every STG.256:
 // 16 extra IMAD.MOV per iteration at NPT = 8, 13 % of the loop's instructions).
-template <int VEC, int NPT, int POLICY, int SYNC, int MODE, int OUT = 0, bool AL = false, bool IL = false,
-          bool PP = false>
-__device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uint32_t bar_threads,
-                                          uint32_t trace_round, uint64_t ilstride = 0) {
+template <int VEC, int NPT, int MODE, int OUT = 0, bool AL = false, bool PP = false>
+__device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uint32_t bar_threads) {
     constexpr int NV = NPT / VEC;
+    constexpr uint64_t vs = 32ull * VEC;  // elements between a lane's vectors
     const uint64_t base = u.base;
-    const uint64_t vs = IL ? ilstride : 32ull * VEC;  // elements between a lane's vectors
     uint64_t x[NPT];
     // ---- load the NPT states of this lane (read once per unit)
     if constexpr (MODE == FULL) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * vs, x + v * VEC);
-    } else if constexpr (MODE == PARTIAL) {
+    } else {
 #pragma unroll
         for (int v = 0; v < NV; ++v)
 #pragma unroll
             for (int e = 0; e < VEC; ++e) {
-                const uint64_t idx = base + (uint64_t)v * 32 * VEC + e;
+                const uint64_t idx = base + (uint64_t)v * vs + e;
                 x[v * VEC + e] = idx < a.count ? a.state[idx] : 0ull;
             }
-    } else {
-#pragma unroll
-        for (int j = 0; j < NPT; ++j) x[j] = 0;
     }
-    if constexpr (MODE != IDLE) {
-        if (u.jump) {  // time-parallel chunk: jump ahead (c*L + e) steps in one GF(2) mat-vec
+    if (u.jump) {  // time-parallel chunk: jump ahead (c*L + e) steps in one GF(2) mat-vec
 #pragma unroll
-            for (int j = 0; j < NPT; ++j) x[j] = gf2_matvec(u.jump, x[j]);
-        }
+        for (int j = 0; j < NPT; ++j) x[j] = gf2_matvec(u.jump, x[j]);
     }
     uint32_t slot = (uint32_t)(((uint64_t)a.slot0 + u.t_begin) % a.nslots);
     uint64_t *p = a.dst + (uint64_t)slot * a.pitch + base;
     const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
-    // One loop trip: store this iteration (if the unit is active), meet the CTA / cluster
-    // barrier, advance to the next ring slot.  Every unit of a launch makes the same number
-    // of trips (the barriers of SYNC 1 / 2 must match): a shorter last chunk idles through
-    // its surplus trips.  The first trip is peeled so the hot loop has no conditions.
-    auto trip = [&](uint32_t t, bool active, const uint64_t *src) {
-        if constexpr (SYNC == 2) {
-            if (t > 0) cluster_wait();
-        }
+    // One loop trip: store this iteration (if the unit is active), meet the CTA barrier,
+    // advance to the next ring slot.  Every unit of a launch makes the same number of trips
+    // (the barriers must match): a shorter last chunk idles through its surplus trips.  The
+    // first trip is peeled so the hot loop has no conditions.
+    auto trip = [&](bool active, const uint64_t *src) {
         if (active) {
             if constexpr (MODE == FULL) {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     if constexpr (OUT == 0) {
-                        store_vec<VEC, POLICY>(p + v * vs, src + v * VEC);
+                        store_vec<VEC>(p + v * vs, src + v * VEC);
                     } else {
                         uint64_t y[VEC];
 #pragma unroll
                         for (int e = 0; e < VEC; ++e) y[e] = emit<OUT>(src[v * VEC + e]);
-                        store_vec<VEC, POLICY>(p + v * vs, y);
+                        store_vec<VEC>(p + v * vs, y);
                     }
                 }
-            } else if constexpr (MODE == PARTIAL) {
+            } else {
 #pragma unroll
                 for (int v = 0; v < NV; ++v)
 #pragma unroll
                     for (int e = 0; e < VEC; ++e)
-                        if (base + (uint64_t)v * 32 * VEC + e < a.count)
-                            p[v * 32 * VEC + e] = emit<OUT>(src[v * VEC + e]);
+                        if (base + (uint64_t)v * vs + e < a.count) p[v * vs + e] = emit<OUT>(src[v * VEC + e]);
             }
         }
-        if constexpr (SYNC == 1 || SYNC == 3) cta_barrier<AL>(bar_threads);
-        if constexpr (SYNC == 5 || SYNC == 6) {  // CTA barrier every 2 / 4 iterations
-            constexpr uint32_t BI = SYNC == 5 ? 2 : 4;
-            if ((t & (BI - 1)) == BI - 1) cta_barrier<AL>(bar_threads);
-        }
-        if constexpr (SYNC == 3) {
-            // drift diagnostic: CTA-leader timestamps every 64 iterations
-            if ((t & 63) == 0 && bar_threads > 0 && a.trace && threadIdx.x == 0) {
-                unsigned long long ts;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
-                const uint64_t per_round = (a.iters + 63) / 64;
-                a.trace[((uint64_t)blockIdx.x * a.rounds + trace_round) * per_round + (t >> 6)] = ts;
-            }
-        }
-        if constexpr (SYNC == 2) {
-            if constexpr (MODE == PARTIAL) __syncwarp();  // reconverge: the cluster barrier is .aligned
-            cluster_arrive();
-        }
+        cta_barrier<AL>(bar_threads);
         if (++slot == a.nslots) {  // warp-uniform
             slot = 0;
             p -= wrap;
@@ -381,17 +310,15 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
         }
     };
     auto step = [&]() {
-        if constexpr (MODE != IDLE) {
 #pragma unroll
-            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
-        }
+        for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
     };
     const uint32_t t_loop = a.nchunks > 1 ? a.chunk_len : a.iters;
-    const uint32_t t_act = MODE == IDLE ? 0u : u.t_count;
+    const uint32_t t_act = u.t_count;
     uint32_t t = 0;
     if (t_act > 0) {
         if (!u.emit_first) step();
-        trip(0, true, x);
+        trip(true, x);
         t = 1;
     }
     if constexpr (PP && MODE == FULL) {
@@ -399,29 +326,28 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
         for (; t + 1 < t_act; t += 2) {  // the hot loop, two iterations per trip
 #pragma unroll
             for (int j = 0; j < NPT; ++j) y[j] = xorshift64(x[j]);
-            trip(t, true, y);
+            trip(true, y);
 #pragma unroll
             for (int j = 0; j < NPT; ++j) x[j] = xorshift64(y[j]);
-            trip(t + 1, true, x);
+            trip(true, x);
         }
     }
     for (; t < t_act; ++t) {  // the hot loop (PP: the odd last iteration)
         step();
-        trip(t, true, x);
+        trip(true, x);
     }
-    for (; t < t_loop; ++t) trip(t, false, x);  // idle trips (short last chunk, IDLE units)
-    if constexpr (SYNC == 2) cluster_wait();  // balance the last arrive
+    for (; t < t_loop; ++t) trip(false, x);  // idle trips (short last chunk)
     // ---- write the state back (== the unit's last iteration) if this unit ends the launch
     if (u.state_out) {
         if constexpr (MODE == FULL) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(u.state_out + base + (uint64_t)v * vs, x + v * VEC);
-        } else if constexpr (MODE == PARTIAL) {
+            for (int v = 0; v < NV; ++v) store_vec<VEC>(u.state_out + base + (uint64_t)v * vs, x + v * VEC);
+        } else {
 #pragma unroll
             for (int v = 0; v < NV; ++v)
 #pragma unroll
                 for (int e = 0; e < VEC; ++e) {
-                    const uint64_t idx = base + (uint64_t)v * 32 * VEC + e;
+                    const uint64_t idx = base + (uint64_t)v * vs + e;
                     if (idx < a.count) u.state_out[idx] = x[v * VEC + e];
                 }
         }
@@ -453,7 +379,7 @@ __device__ __forceinline__ Unit make_unit(const BatchArgs &a, uint64_t unit, uin
 }
 
 // AL: use the .aligned CTA barrier in rounds where the CTA is uniform (see cta_barrier).
-template <int VEC, int NPT, int POLICY, int SYNC, int OUT = 0, bool AL = false, bool IL = false, bool PP = false>
+template <int VEC, int NPT, int OUT = 0, bool AL = false, bool PP = false>
 __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
     static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
     constexpr uint64_t PIECE = 32ull * NPT;
@@ -467,23 +393,13 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
         // unit index of this CTA's warp 0 in round r; the CTA's warps hold consecutive units
         const uint64_t first = a.order ? ((uint64_t)blockIdx.x * a.rounds + r) * wpb : (uint64_t)r * nwarps + cta_warp0;
         const uint64_t unit = first + (warp - cta_warp0);
-        if (unit >= nunits) {  // warp-uniform
-            if constexpr (SYNC == 2) {
-                Unit u = make_unit<NPT, VEC>(a, 0, lane);
-                u.state_out = nullptr;
-                u.t_count = a.nchunks <= 1 ? a.iters : a.chunk_len;
-                run_piece<VEC, NPT, POLICY, SYNC, IDLE, OUT>(a, u, 0, r);
-                continue;
-            } else {
-                break;
-            }
-        }
+        if (unit >= nunits) break;  // warp-uniform: a suffix of the CTA's warps
         const Unit u = make_unit<NPT, VEC>(a, unit, lane);
         // warps of this CTA holding a unit in round r: a prefix of the CTA's warps
         const uint32_t bar_threads = 32u * (uint32_t)(nunits - first < wpb ? nunits - first : wpb);
         const uint64_t piece = unit % a.npieces;
         if ((piece + 1) * PIECE <= a.count) {
-            if constexpr (AL && (SYNC == 1 || SYNC == 3 || SYNC == 5 || SYNC == 6)) {
+            if constexpr (AL) {
                 // uniform round: every active warp of the CTA has a full piece and the same
                 // trip count (only the last piece can be partial, only the last chunk short)
                 const uint64_t last = first + bar_threads / 32 - 1;
@@ -491,102 +407,16 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
                 const bool has_partial = a.count % PIECE != 0 && pf + (last - first) >= a.npieces - 1;
                 const bool same_trips = a.nchunks <= 1 || first / a.npieces == last / a.npieces ||
                                         last / a.npieces + 1 < a.nchunks;
-                if (!has_partial && same_trips) {
-                    if constexpr (IL) {
-                        // interleave the CTA's vectors over its chunk (contiguous pieces of
-                        // one iteration chunk: natural order, no chunk boundary inside)
-                        if (!a.order && first / a.npieces == last / a.npieces) {
-                            const uint64_t nact = bar_threads / 32;
-                            Unit ui = u;
-                            ui.base = pf * PIECE + ((warp - cta_warp0) * 32 + lane) * VEC;
-                            run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, true, true>(a, ui, bar_threads, r,
-                                                                                    nact * 32 * VEC);
-                            continue;
-                        }
-                    }
-                    run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, true, false, PP>(a, u, bar_threads, r);
-                } else
-                    run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false, false, PP>(a, u, bar_threads, r);
+                if (!has_partial && same_trips)
+                    run_piece<VEC, NPT, FULL, OUT, true, PP>(a, u, bar_threads);
+                else
+                    run_piece<VEC, NPT, FULL, OUT, false, PP>(a, u, bar_threads);
             } else {
-                run_piece<VEC, NPT, POLICY, SYNC, FULL, OUT, false, false, PP>(a, u, bar_threads, r);
+                run_piece<VEC, NPT, FULL, OUT, false, PP>(a, u, bar_threads);
             }
         } else {
-            run_piece<VEC, NPT, POLICY, SYNC, PARTIAL, OUT, false>(a, u, bar_threads, r);
+            run_piece<VEC, NPT, PARTIAL, OUT, false>(a, u, bar_threads);
         }
-    }
-}
-
-// ---------------------------------------------------------------- a2+a3, lean single-path form
-// batch_kernel instantiates several unit paths (full / partial pieces, idle trips, jump
-// starts), and ptxas allocates registers for all of them at once: in its hot loop it copies
-// the eight operands of every 32-B store into a staging octet (16 IMAD.MOV per iteration
-// at NPT = 8).  This kernel has one path only -- every piece full, natural order, no
-// chunks -- which the host guarantees before picking it (count % (32 NPT) == 0): the
-// ping-pong hot loop then needs 10 instead of 34 moves per two iterations at NPT = 8.
-// Every active warp of a CTA runs the same instructions, so the .aligned bar.sync is valid.
-template <int VEC, int NPT, int OUT = 0>
-__global__ void __launch_bounds__(256) batch_kernel_lean(BatchArgs a) {
-    static_assert(NPT % VEC == 0, "NPT must be a multiple of VEC");
-    constexpr int NV = NPT / VEC;
-    constexpr uint64_t PIECE = 32ull * NPT;
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t wpb = blockDim.x >> 5;
-    const uint64_t cta_warp0 = (uint64_t)blockIdx.x * wpb;
-    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
-    for (uint32_t r = 0; r < a.rounds; ++r) {
-        const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
-        const uint64_t unit = first + (warp - cta_warp0);
-        if (unit >= a.npieces) break;  // warp-uniform: a suffix of the CTA's warps
-        const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - first < wpb ? a.npieces - first : wpb);
-        const uint64_t base = unit * PIECE + (uint64_t)lane * VEC;
-        uint64_t x[NPT], y[NPT];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
-        uint32_t slot = (uint32_t)(a.slot0 % a.nslots);
-        uint64_t *p = a.dst + (uint64_t)slot * a.pitch + base;
-        auto put = [&](const uint64_t *src) {  // store one iteration, barrier, next slot
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                if constexpr (OUT == 0) {
-                    store_vec<VEC, 0>(p + v * 32 * VEC, src + v * VEC);
-                } else {
-                    uint64_t z[VEC];
-#pragma unroll
-                    for (int q = 0; q < VEC; ++q) z[q] = emit<OUT>(src[v * VEC + q]);
-                    store_vec<VEC, 0>(p + v * 32 * VEC, z);
-                }
-            }
-            cta_barrier<true>(bar_threads);
-            if (++slot == a.nslots) {
-                slot = 0;
-                p -= wrap;
-            } else {
-                p += a.pitch;
-            }
-        };
-        uint32_t t = 0;
-        if (a.first_is_state && a.iters > 0) {  // iteration 0 of a run: the seeds themselves
-            put(x);
-            t = 1;
-        }
-#pragma unroll 1
-        for (; t + 1 < a.iters; t += 2) {  // the hot loop: ping-pong x -> y -> x
-#pragma unroll
-            for (int j = 0; j < NPT; ++j) y[j] = xorshift64(x[j]);
-            put(y);
-#pragma unroll
-            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(y[j]);
-            put(x);
-        }
-        if (t < a.iters) {
-#pragma unroll
-            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
-            put(x);
-        }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
     }
 }
 
@@ -605,7 +435,7 @@ __global__ void __launch_bounds__(256) batch_kernel_lean(BatchArgs a) {
 // one unit is read back by the thread that wrote it: a weak load is enough (same-thread
 // program order, PTX memory model) -- and measured faster than a .cg (LDG.STRONG.GPU)
 // load or prefetching the next unit's state during the current one (exp21).  CTA barrier
-// every iteration as in SYNC 1.
+// every iteration as in batch_kernel.
 __device__ __forceinline__ void ld_v4_wk(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
     asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
 }
@@ -634,7 +464,7 @@ __device__ __forceinline__ void epoch_unit(const BatchArgs &a, uint64_t *x, uint
                 uint64_t y[VEC];
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) y[q] = emit<OUT>(x[v * VEC + q]);
-                store_vec<VEC, 0>(p + v * 32 * VEC, y);
+                store_vec<VEC>(p + v * 32 * VEC, y);
             }
         } else {
 #pragma unroll
@@ -705,7 +535,7 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
                 else
                     epoch_unit<VEC, NPT, OUT, true, false>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
 #pragma unroll
-                for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+                for (int v = 0; v < NV; ++v) store_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
             } else {  // the ragged last piece
 #pragma unroll
                 for (int v = 0; v < NV; ++v)
@@ -725,170 +555,6 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
             }
         }
     }
-}
-
-// ---------------------------------------------------------------- a2+a3 with TMA bulk stores
-// Same work decomposition (VEC = 2), but each iteration's piece is staged in shared
-// memory (STS.128, same lane layout) and written to HBM by ONE bulk async copy per warp
-// (cp.async.bulk.global.shared::cta, 32*NPT*8 contiguous bytes): the SMs issue 1 store
-// instruction per piece instead of NPT/2, the copy engine of the SM forms the DRAM bursts.
-// A ring of STAGES smem buffers per warp lets STAGES-1 bulk copies stay in flight; lane 0
-// waits (wait_group.read) before its stage is overwritten.  Partial pieces fall back to
-// the predicated STG path.
-template <int NPT, int STAGES>
-__device__ __forceinline__ void run_piece_tma(const BatchArgs &a, uint64_t piece, uint32_t lane, uint64_t *wbuf) {
-    constexpr int NV = NPT / 2;
-    constexpr uint32_t BYTES = 32u * NPT * 8u;
-    const uint64_t base = piece * 32ull * NPT + 2ull * lane;
-    uint64_t x[NPT];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) load_vec<2>(a.state + base + (uint64_t)v * 64, x + 2 * v);
-    uint64_t *g = a.dst + (uint64_t)a.slot0 * a.pitch + piece * 32ull * NPT;
-    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
-    uint32_t slot = a.slot0;
-    for (uint32_t t = 0; t < a.iters; ++t) {
-        if (t > 0 || !a.first_is_state) {
-#pragma unroll
-            for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
-        }
-        uint64_t *sb = wbuf + (t % STAGES) * (32 * NPT);
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(STAGES - 1) : "memory");
-        __syncwarp();
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sb + v * 64 + 2 * lane);
-            asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa), "l"(x[2 * v]), "l"(x[2 * v + 1]) : "memory");
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sb);
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa), "n"(BYTES)
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        if (++slot == a.nslots) {
-            slot = 0;
-            g -= wrap;
-        } else {
-            g += a.pitch;
-        }
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) store_vec<2, 0>(a.state + base + (uint64_t)v * 64, x + 2 * v);
-}
-
-template <int NPT, int STAGES>
-__global__ void __launch_bounds__(256) batch_kernel_tma(BatchArgs a) {
-    extern __shared__ __align__(128) uint64_t smem_tma[];
-    constexpr uint64_t PIECE = 32ull * NPT;
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t wib = threadIdx.x >> 5;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    uint64_t *wbuf = smem_tma + (uint64_t)wib * STAGES * PIECE;
-    for (uint32_t r = 0; r < a.rounds; ++r) {
-        const uint64_t piece = (uint64_t)r * nwarps + warp;
-        if (piece >= a.npieces) break;  // warp-uniform
-        if ((piece + 1) * PIECE <= a.count)
-            run_piece_tma<NPT, STAGES>(a, piece, lane, wbuf);
-        else
-            run_piece<2, NPT, 0, 0, PARTIAL>(a, make_unit<NPT, 2>(a, piece, lane), 0, r);
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-
-// ---------------------------------------------------------------- a2+a3: CTA-coherent TMA stores
-// The bench kernel's structure (4 warps per SM, adjacent pieces, CTA barrier every
-// iteration, VEC = 4) with the CTA's whole chunk for an iteration -- wpb x 32 x NPT x 8 B
-// contiguous (8 KiB for v4n8) -- written by ONE bulk async copy from shared memory instead
-// of 32-B STGs.  Per iteration t (stage t mod S):
-//   every lane STS its values into the stage at the chunk's layout, fence.proxy.async;
-//   thread 0 waits until at most S-2 bulk groups are pending reads (so the stage of
-//   iteration t+1 is free); CTA barrier; thread 0 issues cp.async.bulk + commit.
-// Rounds in which the CTA is not uniform (a partial piece, fewer active warps) take the
-// STG path (run_piece).  Natural order only (no chunks / epochs: the host never picks them
-// for stage kernels).
-// PW = true: each warp's lane 0 issues the bulk copy of the warp's own piece (wpb
-// streams per SM) instead of thread 0 issuing the CTA's chunk (one stream per SM).
-template <int NPT, int S, bool PW = false>
-__global__ void __launch_bounds__(256) batch_kernel_tmac(BatchArgs a) {
-    constexpr int VEC = 4, NV = NPT / VEC;
-    constexpr uint64_t PIECE = 32ull * NPT;
-    extern __shared__ __align__(128) uint64_t smem_tmac[];
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t wib = threadIdx.x >> 5;
-    const uint64_t wpb = blockDim.x >> 5;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t cta_warp0 = (uint64_t)blockIdx.x * wpb;
-    const uint64_t chunk_elems = wpb * PIECE;
-    const uint32_t chunk_bytes = (uint32_t)(chunk_elems * sizeof(uint64_t));
-    const uint64_t wrap = (uint64_t)(a.nslots - 1) * a.pitch;
-    for (uint32_t r = 0; r < a.rounds; ++r) {
-        const uint64_t first = (uint64_t)r * nwarps + cta_warp0;
-        const uint64_t unit = first + wib;
-        if (unit >= a.npieces) break;  // warp-uniform
-        const uint32_t bar_threads = 32u * (uint32_t)(a.npieces - first < wpb ? a.npieces - first : wpb);
-        const bool uniform = bar_threads == blockDim.x && (first + wpb) * PIECE <= a.count;
-        if (!uniform) {  // STG path (partial piece / fewer warps in the round)
-            const Unit u = make_unit<NPT, VEC>(a, unit, lane);
-            if ((unit + 1) * PIECE <= a.count)
-                run_piece<VEC, NPT, 0, 1, FULL, 0, false>(a, u, bar_threads, r);
-            else
-                run_piece<VEC, NPT, 0, 1, PARTIAL, 0, false>(a, u, bar_threads, r);
-            continue;
-        }
-        const uint64_t base = unit * PIECE + (uint64_t)lane * VEC;
-        uint64_t x[NPT];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
-        uint32_t slot = a.slot0;
-        uint64_t *g = a.dst + (uint64_t)slot * a.pitch + first * PIECE;  // the CTA's chunk
-        for (uint32_t t = 0; t < a.iters; ++t) {
-            if (t > 0 || !a.first_is_state) {
-#pragma unroll
-                for (int j = 0; j < NPT; ++j) x[j] = xorshift64(x[j]);
-            }
-            uint64_t *sb = smem_tmac + (uint64_t)(t % S) * chunk_elems + (uint64_t)wib * PIECE;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sb + v * 32 * VEC + lane * VEC);
-                asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa), "l"(x[v * VEC]), "l"(x[v * VEC + 1]) : "memory");
-                asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(sa + 16), "l"(x[v * VEC + 2]), "l"(x[v * VEC + 3])
-                             : "memory");
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const bool issuer = PW ? lane == 0 : threadIdx.x == 0;
-            if (issuer) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - 2) : "memory");
-            cta_barrier<true>(bar_threads);
-            if (issuer) {
-                if constexpr (PW) {
-                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sb);
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g + wib * PIECE),
-                                 "r"(sa), "n"((uint32_t)(PIECE * 8)) : "memory");
-                } else {
-                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_tmac + (uint64_t)(t % S) * chunk_elems);
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa),
-                                 "r"(chunk_bytes) : "memory");
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-            if (++slot == a.nslots) {
-                slot = 0;
-                g -= wrap;
-            } else {
-                g += a.pitch;
-            }
-        }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) store_vec<VEC, 0>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
-        // the next round (or the STG path) reuses the stages: drain the pending reads
-        if (PW ? lane == 0 : threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        cta_barrier<true>(bar_threads);
-    }
-    if (PW ? lane == 0 : threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace prngk

@@ -106,8 +106,10 @@ static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, uint64_t T_a
         }
         if (j + 2 < nb) rc = gen(j + 2);
     }
-    cudaStreamSynchronize(h->s_gen);
-    for (auto &e : ev) cudaEventDestroy(e);
+    const cudaError_t es = cudaStreamSynchronize(h->s_gen);
+    for (auto &e : ev)
+        if (e) cudaEventDestroy(e);
+    if (!rc && es != cudaSuccess) rc = set_err(err, PRNG_ECUDA, "generation stream: %s", cudaGetErrorString(es));
     if (rc) {
         h->poisoned = true;
         return rc;
@@ -248,8 +250,12 @@ int prng_detail::generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void
         h->poisoned = true;
         return rc;
     }
-    cudaStreamSynchronize(h->s_gen);
+    const cudaError_t es = cudaStreamSynchronize(h->s_gen);
     cleanup();
+    if (es != cudaSuccess) {
+        h->poisoned = true;
+        return set_err(err, PRNG_ECUDA, "generation stream: %s", cudaGetErrorString(es));
+    }
     h->pos = pos0 + numiter;
     h->wall_s += now_s() - t0;
     return PRNG_OK;
@@ -286,52 +292,57 @@ int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_
     const uint64_t nb = (numiter + T - 1) / T, pitch = h->buf_pitch, pos0 = h->pos;
     auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
     const int R = 4;
-    cudaEvent_t ev_gen[R], ev_cp[R];
-    for (int i = 0; i < R; ++i) {
-        cudaEventCreateWithFlags(&ev_gen[i], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming);
-    }
+    cudaEvent_t ev_gen[R] = {}, ev_cp[R] = {};
     int rc = PRNG_OK;
+    // every CUDA call of the pipeline is checked: a failed record / wait would otherwise let
+    // a copy run before its generation (or a generation overwrite a half still being read)
+    auto chk = [&](cudaError_t e, const char *what) -> int {
+        e = fault_point(h, e);
+        if (e == cudaSuccess) return PRNG_OK;
+        return set_err(err, e == cudaErrorMemoryAllocation ? PRNG_ENOMEM : PRNG_ECUDA, "%s: %s", what,
+                       cudaGetErrorString(e));
+    };
+    for (int i = 0; i < R && !rc; ++i) {
+        rc = chk(cudaEventCreateWithFlags(&ev_gen[i], cudaEventDisableTiming), "cudaEventCreate");
+        if (!rc) rc = chk(cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
     const double t0 = now_s();
     for (uint64_t j = 0; j < nb && !rc; ++j) {
         // gen(j) into device half j%2, after copy(j-2) has drained it (WAR, A15)
-        if (j >= 2 && cudaStreamWaitEvent(h->s_gen, ev_cp[(j - 2) % R], 0) != cudaSuccess) {
-            rc = set_err(err, PRNG_ECUDA, "cudaStreamWaitEvent");
+        if (j >= 2 && (rc = chk(cudaStreamWaitEvent(h->s_gen, ev_cp[(j - 2) % R], 0), "cudaStreamWaitEvent(gen)")))
             break;
-        }
         rc = launch_batch(h, h->d_buf, pitch, 2 * T, (j & 1) * T, iters_of(j), pos0 + j * T == 0, h->s_gen, err);
         if (rc) break;
-        cudaEventRecord(ev_gen[j % R], h->s_gen);
+        if ((rc = chk(cudaEventRecord(ev_gen[j % R], h->s_gen), "cudaEventRecord(gen)"))) break;
         // copy(j): rows (pos0 + j*T + t) mod dst_rows, split where the host ring wraps
-        cudaStreamWaitEvent(h->s_copy, ev_gen[j % R], 0);
+        if ((rc = chk(cudaStreamWaitEvent(h->s_copy, ev_gen[j % R], 0), "cudaStreamWaitEvent(copy)"))) break;
         if ((rc = prof_begin(h, h->s_copy, PRNG_EV_READ_BUFFER, err))) break;
         uint64_t t = 0;
         while (t < iters_of(j)) {
             const uint64_t r0 = (j * T + t) % dst_rows;  // destination row of call iteration j*T + t
             const uint64_t nrows = std::min<uint64_t>(iters_of(j) - t, dst_rows - r0);
-            const cudaError_t e = cudaMemcpy2DAsync(dst + r0 * dst_pitch, dst_pitch * sizeof(uint64_t),
-                                                    h->d_buf + ((j & 1) * T + t) * pitch, pitch * sizeof(uint64_t), row,
-                                                    nrows, cudaMemcpyDeviceToHost, h->s_copy);
-            if (e != cudaSuccess) {
-                rc = set_err(err, PRNG_ECUDA, "cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
-                break;
-            }
+            rc = chk(cudaMemcpy2DAsync(dst + r0 * dst_pitch, dst_pitch * sizeof(uint64_t),
+                                       h->d_buf + ((j & 1) * T + t) * pitch, pitch * sizeof(uint64_t), row, nrows,
+                                       cudaMemcpyDeviceToHost, h->s_copy),
+                     "cudaMemcpy2DAsync");
+            if (rc) break;
             t += nrows;
         }
         if (rc) break;
         if ((rc = prof_end(h, h->s_copy, err))) break;
-        cudaEventRecord(ev_cp[j % R], h->s_copy);
+        if ((rc = chk(cudaEventRecord(ev_cp[j % R], h->s_copy), "cudaEventRecord(copy)"))) break;
         // keep at most two batches in flight per stream (the event ring has R = 4 entries)
-        if (j >= 2) cudaEventSynchronize(ev_cp[(j - 2) % R]);
+        if (j >= 2 && (rc = chk(cudaEventSynchronize(ev_cp[(j - 2) % R]), "cudaEventSynchronize"))) break;
     }
-    cudaStreamSynchronize(h->s_gen);
-    const cudaError_t e = cudaStreamSynchronize(h->s_copy);
+    const cudaError_t eg = cudaStreamSynchronize(h->s_gen);
+    const cudaError_t ec = cudaStreamSynchronize(h->s_copy);
     for (int i = 0; i < R; ++i) {
-        cudaEventDestroy(ev_gen[i]);
-        cudaEventDestroy(ev_cp[i]);
+        if (ev_gen[i]) cudaEventDestroy(ev_gen[i]);
+        if (ev_cp[i]) cudaEventDestroy(ev_cp[i]);
     }
     if (registered_here) cudaHostUnregister(dst);
-    if (!rc && e != cudaSuccess) rc = set_err(err, PRNG_ECUDA, "copy stream: %s", cudaGetErrorString(e));
+    if (!rc) rc = chk(eg, "generation stream");
+    if (!rc) rc = chk(ec, "copy stream");
     if (rc) {
         h->poisoned = true;
         return rc;

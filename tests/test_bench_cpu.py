@@ -36,11 +36,12 @@ def _check(line, n_gpus):
     assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["cpu_baseline"]["cpu_model"] and "numiter=64" in line["cpu_baseline"]["sample"]
 
 
 def test_reference_arm_single_process():
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "3",
-                        "--numrn-per-gpu", "65536"], cwd=ROOT, capture_output=True, text=True, timeout=300)
+                        "--numrn-total", "65536"], cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     lines = _lines(r.stdout)
     assert len(lines) == 1
@@ -50,13 +51,38 @@ def test_reference_arm_single_process():
 @pytest.mark.parametrize("world", [2, 4])
 def test_reference_arm_multi_rank_rank0_only(world):
     """torchrun with N ranks (the driver's launch for N > 1): rank 0 alone prints one line,
-    every rank exits 0, n_gpus = N and the sample covers N x numrn-per-gpu work-items."""
+    every rank exits 0, n_gpus = N, and the line names the same workload as our arm."""
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
                         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus",
-                        str(world), "--impl", "reference", "--steps", "1", "--warmup", "3", "--numrn-per-gpu", "65536"],
+                        str(world), "--impl", "reference", "--steps", "1", "--warmup", "3", "--numrn-total", "65536"],
                        cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     lines = _lines(r.stdout)
     assert len(lines) == 1
     _check(lines[0], world)
-    assert f"numrn={65536 * world}" in lines[0]["config"]["workload"]
+    assert lines[0]["config"]["numrn"] == 65536 and "config 4" in lines[0]["config"]["workload"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_workload_is_the_baseline_config(world):
+    """bench.py's default workload at N GPUs: config 2 / 3 on one GPU (2^24 x 1000), config 4
+    (2^28 TOTAL x 1000, strong scaling, 2^28 / N per rank) and config 5 (e2e 2^28 x 100) on
+    N > 1 -- what the driver's SCALE runs measure (VERDICT r1 "next" #2)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    W = bench.workload(0, 0, 0, world)
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        configs = json.load(f)["configs"]
+    if world == 1:
+        assert (W["numrn"], W["numiter"], W["e2e_numiter"], W["per_gpu"]) == (1 << 24, 1000, 1000, 1 << 24)
+        assert W["workload"].startswith("BASELINE config 2") and W["e2e_workload"].startswith("BASELINE config 3")
+        assert "numrn=2^24" in configs[1] and "numiter=1000" in configs[1]
+    else:
+        assert (W["numrn"], W["numiter"], W["e2e_numiter"]) == (1 << 28, 1000, 100)
+        assert W["per_gpu"] == (1 << 28) // world and W["scaling"] == "strong"
+        assert W["workload"].startswith("BASELINE config 4") and f"({(1 << 28) // world} per GPU)" in W["workload"]
+        assert W["e2e_workload"].startswith("BASELINE config 5") and "numiter=100" in W["e2e_workload"]
+        assert "numrn=2^28" in configs[3] and "numiter=100" in configs[4]
+    # an explicit off-config shape is labelled as such
+    assert not bench.workload(1 << 20, 0, 0, world)["workload"].startswith("BASELINE")

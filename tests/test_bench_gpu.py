@@ -12,8 +12,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SMALL = ["--numrn-per-gpu", str(1 << 22), "--numiter", "200", "--steps", "2", "--warmup", "3", "--no-cpu",
-         "--no-probes"]
+SMALL = ["--numrn-total", str(1 << 22), "--numiter", "200", "--e2e-numiter", "200", "--steps", "2", "--warmup",
+         "3", "--no-cpu", "--no-probes", "--sustained-steps", "3"]
 
 
 def _free_port():
@@ -63,5 +63,32 @@ def test_bench_two_ranks_share_one_gpu():
     lines = _lines(r.stdout)
     assert len(lines) == 1  # rank 0 alone prints
     b = lines[0]
-    assert b["n_gpus"] == 2 and b["metric"] == _metric() and b["scaling"] == "weak" and b["value"] > 0
-    assert b["config"]["numrn"] == 2 * (1 << 22) and b["config"]["parallelism"] == "gid-shard2"
+    assert b["n_gpus"] == 2 and b["metric"] == _metric() and b["scaling"] == "strong" and b["value"] > 0
+    assert b["config"]["numrn"] == 1 << 22 and b["config"]["per_gpu"] == 1 << 21
+    assert b["config"]["parallelism"] == "gid-shard2"
+
+
+@pytest.mark.slow
+def test_bench_two_ranks_default_is_config4_and_5():
+    """The driver's N = 2 launch with the DEFAULT workload (2 ranks sharing the one GPU over
+    gloo): device-only BASELINE config 4 (2^28 total, 2^27 per rank x 1000), e2e config 5
+    (2^28 x 100), and the e2e roofline against the all-ranks-concurrent D2H probe."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+                        "--dist-backend", "gloo", "--device-mod", "1", "--steps", "2", "--warmup", "3",
+                        "--sustained-steps", "2", "--e2e-steps", "1", "--e2e-warmup", "0", "--no-cpu"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = _lines(r.stdout)
+    assert len(lines) == 1
+    b = lines[0]
+    assert b["n_gpus"] == 2 and b["scaling"] == "strong"
+    assert b["config"]["numrn"] == 1 << 28 and b["config"]["per_gpu"] == 1 << 27 and b["config"]["numiter"] == 1000
+    assert b["config"]["workload"].startswith("BASELINE config 4")
+    e = b["e2e"]
+    assert e["workload"].startswith("BASELINE config 5") and e["numiter"] == 100
+    assert e["d2h_bytes_per_step"] == 8 * (1 << 28) * 100
+    pr = b["probes"]
+    assert len(pr["d2h_pinned_concurrent_gbs_per_rank"]) == 2
+    assert e["roofline"]["peak"] == pytest.approx(pr["d2h_pinned_concurrent_gbs_aggregate"])
+    assert "all 2 rank(s) at once" in e["roofline"]["peak_source"]

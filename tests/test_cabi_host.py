@@ -76,7 +76,8 @@ def test_null_handle_calls_fail_cleanly():
 def test_variants_named():
     n = P.prng_kernel_variants()
     names = [P.prng_kernel_variant_name(i) for i in range(n)]
-    assert names[0] == "auto" and {"v4n4s1", "v4n8s1", "v2n4s1"} <= set(names) and len(set(names)) == n
+    assert names == ["auto", "v4n8s1a", "v4n4s1p", "v4n8s1", "v4n16s1", "v2n32s1", "v2n4s1", "v4n4s1"]
+    assert n <= 12  # the product library carries no experiment variants
     assert P.prng_kernel_variant_name(n) is None
     assert [P.prng_event_name(i) for i in range(4)] == list(P.EV_NAMES)
 
@@ -162,3 +163,47 @@ def test_prof_calc_properties(evs, shift):
         cover[int(a):int(b)] += 1
     if cover.max(initial=0) <= 2:
         assert r["effective"] == pytest.approx(total - np.triu(r["overlap"]).sum())
+
+
+# ---------------------------------------------------------------- built-in sinks (plain host C)
+def _sink_call(name, user, iter_begin, iters, gid_begin, count, data):
+    f = getattr(P.lib(), name)
+    return f(ctypes.cast(ctypes.pointer(user), ctypes.c_void_p), iter_begin, iters, gid_begin, count,
+             data.ctypes.data_as(P.P64))
+
+
+def test_sink_copy_checks_gid_and_iteration_range():
+    """prng_sink_copy writes row k - iter_offset, columns gid - gid_offset; a batch whose gids
+    or iterations fall outside the caller's array aborts (returns nonzero) untouched."""
+    dst = np.zeros((2, 10), np.uint64)
+    c = P.CopySink(dst.ctypes.data_as(P.P64), 10, 4, 2, 100)
+    data = np.arange(1, 23, dtype=np.uint64)
+    for it0, its, g0, cnt in [(4, 1, 95, 5), (4, 1, 100, 11), (4, 1, 106, 5), (3, 1, 100, 5), (5, 2, 100, 5)]:
+        assert _sink_call("prng_sink_copy", c, it0, its, g0, cnt, data) != 0, (it0, its, g0, cnt)
+    assert not dst.any()
+    assert _sink_call("prng_sink_copy", c, 4, 2, 105, 5, data) == 0
+    assert dst[0, 5:].tolist() == list(range(1, 6)) and dst[1, 5:].tolist() == list(range(6, 11))
+    assert not dst[:, :5].any()
+
+
+def test_sink_digest_folds():
+    """prng_sink_digest: per-iteration XOR, wrapping sum and sum (2 g + 1) x with the global
+    gid, accumulated over calls (shards combine); wsum_out may be NULL."""
+    M = (1 << 64) - 1
+    r = np.random.default_rng(8)
+    data = r.integers(0, 1 << 63, size=2 * 6, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    x, s, w = (np.zeros(3, np.uint64) for _ in range(3))
+    d = P.DigestSink(x.ctypes.data_as(P.P64), s.ctypes.data_as(P.P64), 10, 3, w.ctypes.data_as(P.P64))
+    assert _sink_call("prng_sink_digest", d, 11, 2, 40, 6, data) == 0
+    rows = data.reshape(2, 6).astype(object)
+    for t in range(2):
+        assert int(s[1 + t]) == sum(rows[t]) & M
+        assert int(w[1 + t]) == sum((2 * (40 + j) + 1) * rows[t][j] for j in range(6)) & M
+        xx = 0
+        for v in rows[t]:
+            xx ^= int(v)
+        assert int(x[1 + t]) == xx
+    assert x[0] == s[0] == w[0] == 0
+    assert _sink_call("prng_sink_digest", d, 13, 1, 0, 6, data) != 0   # iteration 13 outside [10, 13)
+    d2 = P.DigestSink(x.ctypes.data_as(P.P64), s.ctypes.data_as(P.P64), 10, 3, None)
+    assert _sink_call("prng_sink_digest", d2, 10, 1, 0, 6, data) == 0   # no weighted output

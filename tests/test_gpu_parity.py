@@ -9,9 +9,10 @@ import oracle
 import paper_1609_01257_b200 as P
 from workloads import RAGGED_N, SEED_PARITY, SPEC_GRID_I, SPEC_GRID_N, sample_points, shard_range
 
-# variants compiled with the NEXT-3 scrambled-output instantiation (prng_engine.cu VS(...))
-STAR_NAMES = ("v4n4s1", "v2n8s1", "v2n16s1", "v4n8s1", "v2n4s1", "v4n16s1", "v2n32s1", "v4n8s1a", "v4n4s1a",
-              "v4n8s1p", "v4n4s1p", "v4n8s1l", "v4n4s1l")
+# every kernel variant the library compiles (prng_engine.cu kVariants); each has the NEXT-3
+# scrambled-output and the epoch-order instantiations
+ALL_NAMES = ("auto", "v4n8s1a", "v4n4s1p", "v4n8s1", "v4n16s1", "v2n32s1", "v2n4s1", "v4n4s1")
+STAR_NAMES = ALL_NAMES[1:]
 
 
 def _kid(name):
@@ -184,12 +185,11 @@ def test_autotune_then_parity():
     assert np.array_equal(out, oracle.stream(n, i, SEED_PARITY))
 
 
-@pytest.mark.parametrize("kv", range(56))
-def test_every_variant_device_only_wrapping_ring(kv):
+@pytest.mark.parametrize("kname", ALL_NAMES)
+def test_every_variant_device_only_wrapping_ring(kname):
     """Each kernel variant through the device-only ring path (grid-strided rounds, ring
     wrap-around inside one launch), vs the oracle at the ring slots and the state."""
-    if kv >= P.prng_kernel_variants():
-        pytest.skip("no such variant")
+    kv = _kid(kname)
     n, i = 200003, 11
     h = P.prng_create(n, 9)
     try:
@@ -205,50 +205,6 @@ def test_every_variant_device_only_wrapping_ring(kv):
         assert np.array_equal(P.prng_read_state(h, n), want[-1])
     finally:
         P.prng_destroy(h)
-
-
-@pytest.mark.slow
-def test_full_size_config2_sampled():
-    """BASELINE config 2 in bench.py's launch configuration (n = 2^24, numiter = 1000,
-    device only, default variant and ring): every output of the last ring slots at sampled
-    gids, and the final state at sampled gids, vs the oracle's random-access form."""
-    n, i = 1 << 24, 1000
-    h = P.prng_create(n, 0)
-    try:
-        P.prng_init(h)
-        P.prng_generate(h, i)
-        _, pitch, slots, first, end = P.prng_device_ring(h)
-        g, k = sample_points(n, i, 2000, rng_seed=99)
-        st = P.prng_read_state(h, n)
-        for gg in g[:500]:
-            assert int(st[gg]) == oracle.sample(int(gg), i - 1, 0)
-        for kk in sorted({i - 1, i - slots, i - slots // 2}):
-            row = P.prng_read_slot(h, (first + kk) % slots, n)
-            for gg in g[:300]:
-                assert int(row[gg]) == oracle.sample(int(gg), kk, 0)
-        # one whole slot: every gid at the last iteration equals the state
-        assert np.array_equal(P.prng_read_slot(h, (first + i - 1) % slots, n), st)
-    finally:
-        P.prng_destroy(h)
-
-
-@pytest.mark.slow
-def test_full_width_e2e_digests():
-    """BASELINE config 3 in full (n = 2^24, 1000 iterations, end to end through the default
-    O2 pipeline: 134 GB over the host link) with per-iteration XOR / sum digests over every
-    output vs the oracle's digests (threaded over gid shards)."""
-    n, i = 1 << 24, 1000
-    xo = np.zeros(i, np.uint64)
-    so = np.zeros(i, np.uint64)
-    d = P.DigestSink(xo.ctypes.data_as(P.P64), so.ctypes.data_as(P.P64), 0, i)
-    h = P.prng_create(n, SEED_PARITY)
-    try:
-        P.prng_init(h)
-        P.prng_generate(h, i, P.SINK_DIGEST, d)
-    finally:
-        P.prng_destroy(h)
-    wx, ws = _oracle_digest_threads(n, i, SEED_PARITY)
-    assert np.array_equal(xo, wx) and np.array_equal(so, ws)
 
 
 # ---------------------------------------------------------------- errors and causality
@@ -372,16 +328,19 @@ def test_star_output_all_paths(kname):
         P.prng_destroy(h)
 
 
-def test_star_output_rejects_other_variants():
+def test_star_output_any_variant_any_order():
+    """Every variant has the scrambled-output instantiation: OUTPUT = 1 is accepted before
+    or after PRNG_OPT_KERNEL, and out-of-range values are still rejected."""
     h = P.prng_create(64, 0)
     try:
-        P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid("v2n4"))
-        with pytest.raises(P.PrngError):
+        for name in ALL_NAMES:
+            P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 0)
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid(name))
             P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
-        P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid("v2n4s1"))
-        P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
-        with pytest.raises(P.PrngError):  # and the other order
-            P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid("t2n8"))
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, 0)
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid(name))
+        with pytest.raises(P.PrngError):
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, len(ALL_NAMES))
     finally:
         P.prng_destroy(h)
 
@@ -408,12 +367,12 @@ def test_time_parallel_device_only(n, i):
 
 
 @pytest.mark.parametrize("batch", [0, 700, 1])
-@pytest.mark.parametrize("kv", [0, 1, 4, 12])
-def test_time_parallel_e2e_and_split(batch, kv):
+@pytest.mark.parametrize("kname", ["auto", "v4n8s1a", "v2n4s1", "v2n32s1"])
+def test_time_parallel_e2e_and_split(batch, kname):
     """Chunked batches (alternating e = 0 / 1 jump offsets), split calls, several variants."""
     n, i = 1000, 3000
     want = oracle.stream(n, i, 17)
-    got = run_e2e(n, i, 17, batch=batch, kernel=kv, calls=[1000, 1313, 687])
+    got = run_e2e(n, i, 17, batch=batch, kernel=_kid(kname), calls=[1000, 1313, 687])
     assert np.array_equal(got, want)
 
 
@@ -435,7 +394,7 @@ def test_time_parallel_off_is_identical():
 
 @pytest.mark.parametrize("order", [0, 1])
 @pytest.mark.parametrize("chunk", [0, 1, 37, 300])
-@pytest.mark.parametrize("kname", ["v4n4s1", "v2n8", "v2n4s1"])
+@pytest.mark.parametrize("kname", ["v4n4s1", "v4n8s1a", "v2n4s1"])
 def test_forced_chunks_and_piece_order(kname, chunk, order):
     """PRNG_OPT_CHUNK_ITERS (jump-started chunks at any numrn) and PRNG_OPT_PIECE_ORDER
     (CTA-blocked dealing) change only the work order: every output, split calls included,
@@ -581,8 +540,8 @@ def test_auto_kernel_at_bench_shape(n, name):
 
 def test_forced_chunks_device_only_bench_shape():
     """Forced chunks + CTA-blocked order at the bench width (2^24), device-only into a
-    torch buffer: every iteration's XOR and wrapping sum of all 2^24 outputs (folded on the
-    GPU) vs the oracle's per-iteration digests, and the final state."""
+    torch buffer: every iteration's XOR, wrapping sum and gid-weighted sum of all 2^24
+    outputs (folded on the GPU) vs the oracle, and the final state element by element."""
     import torch
     n, i = 1 << 24, 48
     h = P.prng_create(n, SEED_PARITY)
@@ -593,20 +552,16 @@ def test_forced_chunks_device_only_bench_shape():
         P.prng_init(h)
         P.prng_generate_device(h, i, buf.data_ptr(), n, i, 0)
         torch.cuda.synchronize()
-        got_s = [int(v) & ((1 << 64) - 1) for v in buf.sum(dim=1).tolist()]  # int64 sum wraps mod 2^64
-        v, m = buf.clone(), n
-        while m > 1:
-            h2 = m // 2
-            v[:, :h2] ^= v[:, m - h2:m]
-            m -= h2
-        got_x = [int(x) & ((1 << 64) - 1) for x in v[:, 0].tolist()]
+        w = _weights(0, n)
+        got = [_gpu_folds(buf[k], w) for k in range(i)]
         last = buf[-1].cpu().numpy().view(np.uint64)
         st = P.prng_read_state(h, n)
     finally:
         P.prng_destroy(h)
-    wx, ws = _oracle_digest_threads(n, i, SEED_PARITY)
-    assert got_x == [int(x) for x in wx] and got_s == [int(x) for x in ws]
-    assert np.array_equal(st, last)
+    want = _oracle_folds_threads(n, i, SEED_PARITY, last=True)
+    for k in range(i):
+        assert got[k] == (int(want["xor"][k]), int(want["sum"][k]), int(want["wsum"][k])), k
+    assert np.array_equal(last, want["last"]) and np.array_equal(st, want["last"])
 
 
 @pytest.mark.parametrize("slots", [1, 7, 300])
@@ -634,10 +589,10 @@ def test_chunks_never_race_on_a_wrapping_ring(slots, chunk):
 
 
 @pytest.mark.parametrize("out_kind", [0, 1])
-@pytest.mark.parametrize("kname", ["v4n8s1l", "v4n4s1l"])
-def test_lean_kernel(kname, out_kind):
-    """The lean single-path kernel (batch_kernel_lean: every piece full, natural order)
-    runs when numrn is a multiple of the piece size.  Even and odd iteration counts,
+@pytest.mark.parametrize("kname", ["v4n8s1a", "v4n4s1p"])
+def test_full_pieces_even_and_odd_iterations(kname, out_kind):
+    """numrn a multiple of the piece size (every round uniform: the .aligned barrier of
+    v4n8s1a, the two-iteration ping-pong loop of v4n4s1p).  Even and odd iteration counts,
     split calls (the first launch starts with the seeds, later ones with a step), end to
     end and device only, both output transforms, and a grid with several rounds per warp,
     vs the oracle."""
@@ -706,103 +661,11 @@ def test_nonblocking_accumulated_profile():
         P.prng_destroy(h)
 
 
-def _oracle_digest_threads(n, i, seed, nthreads=None):
-    """oracle.digest on contiguous gid shards in parallel threads (ctypes releases the GIL);
-    per-iteration XOR and wrapping sum combine across shards."""
-    import os
-    import threading
-    nthreads = nthreads or max(1, len(os.sched_getaffinity(0)))
-    res = [None] * nthreads
-
-    def work(r):
-        b, c = shard_range(n, r, nthreads)
-        res[r] = oracle.digest(n, i, seed, gid_begin=b, count=c) if c else None
-
-    th = [threading.Thread(target=work, args=(r,)) for r in range(nthreads)]
-    [t.start() for t in th]
-    [t.join() for t in th]
-    x = np.zeros(i, np.uint64)
-    s = np.zeros(i, np.uint64)
-    for rr in res:
-        if rr is not None:
-            x ^= rr[0]
-            s += rr[1]
-    return x, s
-
-
 class _DevArray:
     """__cuda_array_interface__ view of library-owned device memory (read-only use)."""
 
     def __init__(self, ptr, shape):
         self.__cuda_array_interface__ = {"data": (ptr, False), "shape": shape, "typestr": "<i8", "version": 3}
-
-
-@pytest.mark.slow
-def test_bench_config_every_ring_slot():
-    """The exact bench.py device-only configuration (numrn = 2^24, numiter = 1000, default
-    kernel and 64 GiB rotating ring, one launch): every output of every iteration still in
-    the ring (the last R = 512 of 1000) folded per iteration into XOR and wrapping sum on
-    the GPU, vs the oracle's digests of the same iterations."""
-    import torch
-    n, i = 1 << 24, 1000
-    h = P.prng_create(n, 0)
-    try:
-        P.prng_init(h)
-        P.prng_generate(h, i)
-        base, pitch, slots, first, end = P.prng_device_ring(h)
-        assert end == i and slots < i
-        ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
-        got_x, got_s = {}, {}
-        for k in range(i - slots, i):
-            row = ring[(first + k) % slots, :n]
-            got_s[k] = int(row.sum().item()) & ((1 << 64) - 1)   # int64 sum wraps mod 2^64
-            v = row.clone()
-            m = v.numel()
-            while m > 1:
-                h2 = m // 2
-                v[:h2] ^= v[m - h2:m]
-                m -= h2
-            got_x[k] = int(v[0].item()) & ((1 << 64) - 1)
-    finally:
-        P.prng_destroy(h)
-    wx, ws = _oracle_digest_threads(n, i, 0)
-    for k in range(i - slots, i):
-        assert got_x[k] == int(wx[k]) and got_s[k] == int(ws[k]), k
-
-
-@pytest.mark.slow
-@pytest.mark.parametrize("lg,name", [(25, "v4n8s1a"), (26, "v4n16s1"), (27, "v2n32s1")])
-def test_config4_rank_shapes_every_ring_slot(lg, name):
-    """BASELINE config 4 at its per-rank shapes (2^28 over 8 / 4 / 2 GPUs = 2^25 / 2^26 /
-    2^27 per rank, 1000 iterations, default 64 GiB ring of 256 / 128 / 64 slots): the
-    kernel the anti-absorption rule runs, and for each iteration still in the ring the XOR
-    and wrapping sum of all its outputs (folded on the GPU) vs the oracle's digests."""
-    import torch
-    n, i = 1 << lg, 1000
-    h = P.prng_create(n, SEED_PARITY)
-    try:
-        P.prng_init(h)
-        P.prng_generate(h, i)
-        assert (P.prng_kernel_variant_name(P.prng_last_launch(h)[0]), P.prng_last_launch(h)[1]) == (name, 0)
-        base, pitch, slots, first, end = P.prng_device_ring(h)
-        ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
-        got = {}
-        for k in range(i - slots, i):
-            row = ring[(first + k) % slots, :n]
-            s_ = int(row.sum().item()) & ((1 << 64) - 1)
-            v = row.clone()
-            m = v.numel()
-            while m > 1:
-                h2 = m // 2
-                v[:h2] ^= v[m - h2:m]
-                m -= h2
-            got[k] = (int(v[0].item()) & ((1 << 64) - 1), s_)
-            del v
-    finally:
-        P.prng_destroy(h)
-    wx, ws = _oracle_digest_threads(n, i, SEED_PARITY)
-    for k in range(i - slots, i):
-        assert got[k] == (int(wx[k]), int(ws[k])), k
 
 
 # ---------------------------------------------------------------- shared host output (north_star e)
@@ -1000,7 +863,7 @@ def test_randomised_configurations():
     r = np.random.default_rng(20261017)
     nvar = P.prng_kernel_variants()
     names = [P.prng_kernel_variant_name(k) for k in range(nvar)]
-    usable = [k for k in range(nvar) if names[k] != "v2n4s1t"]
+    usable = list(range(nvar))
     for trial in range(60):
         n = int(r.choice([1, 2, 3, 31, 64, 100, 1000, 4096, 5003, 20000, 70001]))
         i = int(r.choice([1, 2, 5, 17, 130, 600]))
@@ -1009,7 +872,7 @@ def test_randomised_configurations():
         if mode == P.PRNG_MODE_ZEROCOPY and n % 4:
             mode = P.PRNG_MODE_OVERLAP2
         kv = int(r.choice(usable))
-        star = int((names[kv] in STAR_NAMES or names[kv] == "auto") and r.random() < 0.3)
+        star = int(r.random() < 0.3)
         tp = int(r.random() < 0.8)
         batch = int(r.choice([0, 1, 3, 50]))
         epoch = int(r.choice([0, 0, -1, 1, 7, 64]))
@@ -1050,11 +913,162 @@ def test_randomised_configurations():
             P.prng_destroy(h)
 
 
+
+# ---------------------------------------------------------------- full shapes, order-sensitive
+M64 = (1 << 64) - 1
+
+
+def _oracle_folds_threads(n, i, seed, gid_begin=0, count=None, last=False, nthreads=None):
+    """oracle.folds on contiguous gid shards of [gid_begin, gid_begin + count) in parallel
+    threads (ctypes releases the GIL).  The folds combine across shards: XOR, wrapping sum,
+    and the gid-weighted sum (its weights use the global gid); `last` concatenates."""
+    import os
+    import threading
+    count = n - gid_begin if count is None else count
+    nthreads = nthreads or max(1, len(os.sched_getaffinity(0)))
+    res = [None] * nthreads
+
+    def work(r):
+        b, c = shard_range(count, r, nthreads)
+        res[r] = oracle.folds(n, i, seed, gid_begin=gid_begin + b, count=c, last=last) if c else None
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nthreads)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    out = {"xor": np.zeros(i, np.uint64), "sum": np.zeros(i, np.uint64), "wsum": np.zeros(i, np.uint64)}
+    for rr in res:
+        if rr is not None:
+            out["xor"] ^= rr["xor"]
+            out["sum"] += rr["sum"]
+            out["wsum"] += rr["wsum"]
+    if last:
+        out["last"] = np.concatenate([rr["last"] for rr in res if rr is not None])
+    return out
+
+
+def _gpu_folds(row, weights):
+    """(xor, sum, gid-weighted sum) of one int64 CUDA row; torch's int64 arithmetic wraps
+    mod 2^64 (two's complement), which is the oracle's u64 arithmetic."""
+    s = int(row.sum().item()) & M64
+    w = int((row * weights).sum().item()) & M64
+    v = row.clone()
+    m = v.numel()
+    while m > 1:
+        h2 = m // 2
+        v[:h2] ^= v[m - h2:m]
+        m -= h2
+    return int(v[0].item()) & M64, s, w
+
+
+def _weights(gid_begin, count):
+    import torch
+    return torch.arange(count, dtype=torch.int64, device="cuda") * 2 + (2 * gid_begin + 1)
+
+
+def _device_only_full_shape(numrn_total, gid_begin, count, numiter, seed, expect_kernel=None):
+    """One device-only launch exactly as bench.py runs it (default kernel, default 64 GiB
+    rotating ring): for every iteration still in the ring, the XOR, the wrapping sum and the
+    gid-weighted sum of all its outputs (order-sensitive: a misplaced piece changes it), and
+    the whole last iteration and the final state element by element -- all against the
+    oracle's flat loop over the same gid range."""
+    import torch
+    h = P.prng_create_range(numrn_total, seed, gid_begin, count, 0)
+    try:
+        P.prng_init(h)
+        P.prng_generate(h, numiter)
+        ran, epoch = P.prng_last_launch(h)
+        if expect_kernel is not None:
+            assert (P.prng_kernel_variant_name(ran), epoch) == expect_kernel
+        base, pitch, slots, first, end = P.prng_device_ring(h)
+        assert end == numiter
+        ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
+        w = _weights(gid_begin, count)
+        got = {k: _gpu_folds(ring[(first + k) % slots, :count], w) for k in range(max(0, numiter - slots), numiter)}
+        last = ring[(first + numiter - 1) % slots, :count].cpu().numpy().view(np.uint64).copy()
+        st = P.prng_read_state(h)
+        del ring, w
+    finally:
+        P.prng_destroy(h)
+    want = _oracle_folds_threads(numrn_total, numiter, seed, gid_begin, count, last=True)
+    for k, (x, s, ws) in got.items():
+        assert (x, s, ws) == (int(want["xor"][k]), int(want["sum"][k]), int(want["wsum"][k])), k
+    assert np.array_equal(last, want["last"]), "last iteration differs from the oracle"
+    assert np.array_equal(st, want["last"]), "final state differs from the oracle"
+    # and, by an independent route (the random-access form xs^k(seed64(g))), sampled gids
+    g, k = sample_points(numrn_total, numiter, 200, rng_seed=99, gid_begin=gid_begin, count=count)
+    for gg in g[:200]:
+        assert int(st[gg - gid_begin]) == oracle.sample(int(gg), numiter - 1, seed)
+
+
 @pytest.mark.slow
-def test_bench_config_every_iteration_no_ring():
+def test_config2_bench_shape_order_sensitive():
+    """BASELINE config 2 = the bench step (numrn = 2^24, numiter = 1000, seed 0, the default
+    kernel "auto" -> v4n8s1a, 512-slot ring): every ring slot's three folds, the whole last
+    iteration and the state element by element, vs the oracle."""
+    _device_only_full_shape(1 << 24, 0, 1 << 24, 1000, 0, ("v4n8s1a", 0))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("lg,name", [(25, "v4n8s1a"), (26, "v4n16s1"), (27, "v2n32s1")])
+def test_config4_rank_shapes_order_sensitive(lg, name):
+    """BASELINE config 4 at its per-rank shapes: 2^28 over P = 8 / 4 / 2 ranks gives 2^25 /
+    2^26 / 2^27 gids per rank, 1000 iterations, default 64 GiB ring of 256 / 128 / 64 slots
+    (the anti-absorption rule picks v4n8s1a / v4n16s1 / v2n32s1).  The LAST rank's gid range
+    (up to gid 2^28 - 1), so the global-gid weights and the gid offset are exercised."""
+    n = 1 << lg
+    P_ = (1 << 28) // n
+    b, c = shard_range(1 << 28, P_ - 1, P_)
+    _device_only_full_shape(1 << 28, b, c, 1000, SEED_PARITY, (name, 0))
+
+
+def _e2e_digest_run(numrn_total, gid_begin, count, numiter, seed, mode):
+    """End to end through prng_generate with the digest sink (xor / sum / gid-weighted sum
+    per iteration, folded on the host from the pinned batches) and the final state."""
+    xo, so, wo = (np.zeros(numiter, np.uint64) for _ in range(3))
+    d = P.DigestSink(xo.ctypes.data_as(P.P64), so.ctypes.data_as(P.P64), 0, numiter, wo.ctypes.data_as(P.P64))
+    h = P.prng_create_range(numrn_total, seed, gid_begin, count, 0)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_MODE, mode)
+        P.prng_init(h)
+        P.prng_generate(h, numiter, P.SINK_DIGEST, d)
+        st = P.prng_read_state(h)
+    finally:
+        P.prng_destroy(h)
+    return xo, so, wo, st
+
+
+@pytest.mark.slow
+def test_config3_full_e2e_order_sensitive():
+    """BASELINE config 3 in full: 2^24 x 1000 end to end through the default O2 pipeline
+    (134 GB over the host link); every iteration's three folds and the final state vs the
+    oracle."""
+    n, i = 1 << 24, 1000
+    xo, so, wo, st = _e2e_digest_run(n, 0, n, i, SEED_PARITY, P.PRNG_MODE_OVERLAP2)
+    want = _oracle_folds_threads(n, i, SEED_PARITY, last=True)
+    assert np.array_equal(xo, want["xor"]) and np.array_equal(so, want["sum"]) and np.array_equal(wo, want["wsum"])
+    assert np.array_equal(st, want["last"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("mode", [P.PRNG_MODE_OVERLAP2, P.PRNG_MODE_ZEROCOPY])
+def test_config5_rank_shape_e2e_order_sensitive(mode):
+    """BASELINE config 5 at its per-rank shape: rank 3 of 8 of the 2^28 stream (2^25 gids
+    from gid 3 x 2^25), 100 iterations, end to end through the pinned double buffer (O2) and
+    through zero-copy (O3): every iteration's three folds and the final state vs the oracle
+    over the same gid range (the paper's read / out pipeline)."""
+    n, i = 1 << 28, 100
+    b, c = shard_range(n, 3, 8)
+    xo, so, wo, st = _e2e_digest_run(n, b, c, i, SEED_PARITY, mode)
+    want = _oracle_folds_threads(n, i, SEED_PARITY, b, c, last=True)
+    assert np.array_equal(xo, want["xor"]) and np.array_equal(so, want["sum"]) and np.array_equal(wo, want["wsum"])
+    assert np.array_equal(st, want["last"])
+
+
+@pytest.mark.slow
+def test_config2_every_iteration_no_ring():
     """The bench kernel at the bench shape (2^24 x 1000, one launch, default variant and
     grid) into a 134 GB device buffer with one slot per iteration (no wrap): all 1000
-    iterations folded per iteration (XOR, wrapping sum) on the GPU vs the oracle."""
+    iterations folded on the GPU (XOR, wrapping sum, gid-weighted sum) vs the oracle."""
     import torch
     n, i = 1 << 24, 1000
     free, _ = torch.cuda.mem_get_info()
@@ -1066,19 +1080,136 @@ def test_bench_config_every_iteration_no_ring():
         P.prng_init(h)
         P.prng_generate_device(h, i, buf.data_ptr(), n, i, torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
-        sums = buf.sum(dim=1)  # int64 sums wrap mod 2^64
-        v = buf
-        m = n
-        while m > 1:  # XOR fold along gids, in place, one level per pass
-            h2 = m // 2
-            v[:, :h2] ^= v[:, m - h2:m]
-            m -= h2
-        xors = v[:, 0].clone()
+        w = _weights(0, n)
+        got = [_gpu_folds(buf[k], w) for k in range(i)]
     finally:
         P.prng_destroy(h)
-    got_s = sums.cpu().numpy().view(np.uint64)
-    got_x = xors.cpu().numpy().view(np.uint64)
-    del buf, v
+    del buf
     torch.cuda.empty_cache()
-    wx, ws = _oracle_digest_threads(n, i, 0)
-    assert np.array_equal(got_x, wx) and np.array_equal(got_s, ws)
+    want = _oracle_folds_threads(n, i, 0)
+    for k in range(i):
+        assert got[k] == (int(want["xor"][k]), int(want["sum"][k]), int(want["wsum"][k])), k
+
+
+# ---------------------------------------------------------------- A3: the zero-state fix-up on the GPU
+A3_GID, A3_SEED = 2654435716, 0x236D2904C6FC2D12   # derived in tests/test_oracle_pins.py::_a3_trigger
+
+
+@pytest.mark.parametrize("case", ["e2e_default", "v2n4s1", "epoch", "time_parallel", "star", "zerocopy",
+                                  "device_only"])
+def test_a3_zero_fixup_on_gpu(case):
+    """The seed kernel's 0 -> 1 fix-up (reading A3; PAPER.md P:173 needs
+    nonzero seeds) at the one gid where the raw composition is 0: 2000 gids around it of the
+    2^32 stream, element by element vs the oracle, through the default path, the 16-byte
+    variant, epoch order, time-parallel chunks, the scrambled output, zero-copy and the
+    device-only ring."""
+    n, b, c = 1 << 32, A3_GID - 1000, 2000
+    i = 600 if case == "time_parallel" else 9
+    star = case == "star"
+    want = (oracle.stream_star if star else oracle.stream)(n, i, A3_SEED, gid_begin=b, count=c)
+    plain = oracle.stream(n, i, A3_SEED, gid_begin=b, count=c)
+    assert plain[0, 1000] == 1 and plain[1, 1000] == 1082269761
+    h = P.prng_create_range(n, A3_SEED, b, c, 0)
+    try:
+        if case == "v2n4s1":
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid("v2n4s1"))
+        if case == "star":
+            P.prng_set_option(h, P.PRNG_OPT_OUTPUT, 1)
+        if case == "zerocopy":
+            P.prng_set_option(h, P.PRNG_OPT_MODE, P.PRNG_MODE_ZEROCOPY)
+        if case in ("epoch", "device_only"):
+            P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, i)
+            if case == "epoch":
+                P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, 3)
+                P.prng_set_option(h, P.PRNG_OPT_TIME_PARALLEL, 0)
+            P.prng_init(h)
+            P.prng_generate(h, i)
+            ran, epoch = P.prng_last_launch(h)
+            assert epoch == (3 if case == "epoch" else 0)
+            _, _, R, first, _ = P.prng_device_ring(h)
+            out = np.stack([P.prng_read_slot(h, (first + k) % R) for k in range(i)])
+        else:
+            out = np.zeros((i, c), np.uint64)
+            P.prng_init(h)
+            P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), c, 0, i, b))
+        st = P.prng_read_state(h)
+    finally:
+        P.prng_destroy(h)
+    assert np.array_equal(out, want)
+    assert np.array_equal(st, plain[-1])
+    if not star:
+        assert out[0, 1000] == 1
+
+
+# ---------------------------------------------------------------- ABI robustness
+def test_set_streams_validates_before_touching_the_handle():
+    """prng_set_streams(NULL, NULL) / identical streams: PRNG_EINVAL and the handle keeps its
+    own two streams -- generation afterwards still overlaps and is bit-exact."""
+    import torch
+    n, i = 5000, 12
+    h = P.prng_create(n, 4)
+    try:
+        s = torch.cuda.Stream()
+        for g, c in [(0, 0), (s.cuda_stream, 0), (0, s.cuda_stream), (s.cuda_stream, s.cuda_stream)]:
+            with pytest.raises(P.PrngError) as e:
+                P.prng_set_streams(h, g, c)
+            assert e.value.code == P.PRNG_EINVAL
+        out = np.zeros((i, n), np.uint64)
+        P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 2)
+        P.prng_init(h)
+        P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0))
+        assert np.array_equal(out, oracle.stream(n, i, 4))
+        # valid torch streams are then accepted and used
+        g2, c2 = torch.cuda.Stream(), torch.cuda.Stream()
+        P.prng_set_streams(h, g2.cuda_stream, c2.cuda_stream)
+        P.prng_init(h)
+        P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, 0, i, 0))
+        assert np.array_equal(out, oracle.stream(n, i, 4))
+    finally:
+        P.prng_destroy(h)
+
+
+@pytest.mark.parametrize("fail_at", [1, 2, 3, 4, 5, 9])
+def test_generate_host_failure_poisons_the_handle(fail_at, monkeypatch):
+    """A CUDA call of prng_generate_host that fails (fault injected at the fail_at-th checked
+    call: stream waits, event records, the 2-D copies, event syncs) makes the call return
+    PRNG_ECUDA and poisons the handle (PRNG_ESTATE) instead of returning silently; after
+    prng_init the handle is bit-exact again."""
+    monkeypatch.setenv("PRNG_B200_FAULT_AFTER", str(fail_at))
+    n, i = 3000, 12
+    h = P.prng_create(n, 6)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 2)
+        arr = np.zeros((i, n), np.uint64)
+        P.prng_init(h)
+        with pytest.raises(P.PrngError) as e:
+            P.prng_generate_host(h, i, arr, n, i)
+        assert e.value.code == P.PRNG_ECUDA
+        with pytest.raises(P.PrngError) as e:
+            P.prng_generate_host(h, i, arr, n, i)
+        assert e.value.code == P.PRNG_ESTATE
+        P.prng_init(h)
+        P.prng_generate_host(h, i, arr, n, i)   # the injected fault fired once
+        assert np.array_equal(arr, oracle.stream(n, i, 6))
+    finally:
+        P.prng_destroy(h)
+
+
+def test_binding_checks_host_buffer_sizes():
+    """The Python binding refuses host arrays smaller than what the C side would write."""
+    n = 1000
+    h = P.prng_create(n, 0)
+    try:
+        P.prng_init(h)
+        with pytest.raises(ValueError):
+            P.prng_generate_host(h, 4, np.zeros((3, n), np.uint64), n, 4)       # 3 rows < 4
+        with pytest.raises(ValueError):
+            P.prng_generate_host(h, 2, np.zeros((2, n), np.uint64), n, 2, col_offset=1)
+        with pytest.raises(ValueError):
+            P.prng_read_state(h, n + 1)
+        assert P.prng_get_range(h) == (n, 0, n)
+        arr = np.zeros((2, n), np.uint64)
+        P.prng_generate_host(h, 2, arr, n, 2)
+        assert np.array_equal(arr, oracle.stream(n, 2, 0))
+    finally:
+        P.prng_destroy(h)

@@ -1,8 +1,8 @@
 #!/usr/bin/env python3
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel
-family (CTA-sync, free-running, cluster, TMA bulk-store, time-parallel jump-ahead, epoch
-order, the anti-absorption substitution, star output, zero-copy), checked against the
-oracle.  Run from the repo root on a GPU box:
+family (natural order with the .aligned / non-.aligned barrier, ping-pong loop,
+time-parallel jump-ahead, epoch order, the anti-absorption substitution, star output,
+zero-copy), checked against the oracle.  Run from the repo root on a GPU box:
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py
 """
 import os
@@ -18,17 +18,13 @@ names = [P.prng_kernel_variant_name(i) for i in range(P.prng_kernel_variants())]
 cases = [  # (n, iters, variant, mode, output, device-ring slots, PRNG_OPT_EPOCH_ITERS)
     (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 1000, 0),  # time-parallel chunks (iters >= 512)
     (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 16, 0),    # wrapping ring: epoch order, E = 16
-    (1003, 9, "v2n8s1", P.PRNG_MODE_OVERLAP1, 1, 16, 0),      # star output, ragged n
-    (4100, 7, "v4n8", P.PRNG_MODE_SERIAL, 0, 16, 0),
-    (4096, 5, "v2n8c2", P.PRNG_MODE_OVERLAP2, 0, 16, 0),      # cluster barrier
-    (5000, 6, "t2n8", P.PRNG_MODE_OVERLAP2, 0, 16, 0),        # TMA bulk stores
+    (1003, 9, "v4n4s1", P.PRNG_MODE_OVERLAP1, 1, 16, 0),      # star output, ragged n
+    (4100, 7, "v4n4s1p", P.PRNG_MODE_SERIAL, 0, 16, 0),       # ping-pong hot loop
     (4096, 6, "v2n4s1", P.PRNG_MODE_ZEROCOPY, 0, 16, 0),      # zero-copy
     (70001, 40, "auto", P.PRNG_MODE_OVERLAP2, 1, 16, 7),      # forced epochs, star, ragged
     (1 << 20, 70, "auto", P.PRNG_MODE_OVERLAP2, 0, 64, 0),    # anti-absorption: v2n32s1
     (300000, 9, "v4n8s1a", P.PRNG_MODE_OVERLAP2, 0, 16, 0),   # .aligned barrier in uniform rounds
-    (300000, 9, "v4n8s1ai", P.PRNG_MODE_OVERLAP2, 0, 16, 0),  # interleaved CTA vectors
-    (300000, 9, "c4n8s4", P.PRNG_MODE_OVERLAP2, 0, 16, 0),    # CTA-coherent TMA bulk stores
-    (300000, 9, "w4n8s4", P.PRNG_MODE_OVERLAP2, 0, 16, 0),    # per-warp TMA bulk stores + CTA barrier
+    (300000, 9, "v4n16s1", P.PRNG_MODE_OVERLAP2, 1, 16, 0),   # wide pieces, ragged last piece
 ]
 bad = 0
 for n, it, v, mode, out, slots, epoch in cases:
