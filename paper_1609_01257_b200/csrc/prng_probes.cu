@@ -40,15 +40,14 @@ __global__ void __launch_bounds__(256) store_probe_kernel(uint64_t *p, uint64_t 
 // One-shot fill: CTA b (128 threads) writes the contiguous 16 KiB chunk b with four 32-byte
 // stores per thread and exits (the structure of a framework fill kernel).  The hardware
 // dispatches the CTAs in order, so the write front advances through memory as one compact
-// window; measured the fastest SM write pattern on B200 (tools/experiments_r2/, r2_write.md).
+// window; measured the fastest SM write pattern on B200 (profiles/r2_write_ceiling.md).
 constexpr uint64_t kFillChunk = 2048;  // u64 per CTA
 __global__ void __launch_bounds__(128) fill_probe_kernel(uint64_t *p) {
     const uint64_t base = (uint64_t)blockIdx.x * kFillChunk;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const uint64_t i = base + k * 512 + threadIdx.x * 4;
-        const uint64_t x = mix(i + 1);
-        st4(p + i, x, x ^ 1, x ^ 2, x ^ 3);
+        st4(p + i, mix(i + 1), mix(i + 2), mix(i + 3), mix(i + 4));
     }
 }
 

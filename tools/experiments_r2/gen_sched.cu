@@ -149,6 +149,35 @@ __global__ void __launch_bounds__(256) g2_tile(uint64_t *out, uint64_t *state, u
     if (dummy == 42) state[0] = dummy;
 }
 
+// ---- G3: gid-blocked layout: CTA block b (W warps x 32 x NPT gids = `chunk` u64) writes
+// iteration t of its gids at out + b*T*chunk + t*chunk (each CTA one sequential stream).
+// Grid-stride over blocks (persistent if gridDim < nblocks, one-shot otherwise).
+template <int NPT>
+__global__ void __launch_bounds__(256) g3_blocked(uint64_t *out, uint64_t *state, uint64_t n, uint32_t T) {
+    constexpr int NV = NPT / 4;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t chunk = (uint64_t)blockDim.x * NPT;
+    const uint64_t nblk = n / chunk;
+    for (uint64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const uint64_t wbase = (threadIdx.x >> 5) * 32 * NPT + lane * 4;  // within the block
+        uint64_t x[NPT];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            ld4(state + blk * chunk + wbase + v * 128, x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+        uint64_t *p = out + blk * T * chunk + wbase;
+        for (uint32_t t = 0; t < T; ++t) {
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = xs(x[j]);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) st4(p + v * 128, x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+            p += chunk;
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            st4(state + blk * chunk + wbase + v * 128, x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+    }
+}
+
 __global__ void init_state(uint64_t *s, uint64_t n) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         s[i] = mix(i + 1) | 1;
@@ -187,32 +216,17 @@ int main(int argc, char **argv) {
         fflush(stdout);
     };
     char prm[256];
-    // G1 persistent (1 CTA of 4 warps per SM, NPT 8) with pacing
-    for (int pace : {0, 2, 4, 8, 16}) {
-        snprintf(prm, sizeof prm, "\"npt\": 8, \"warps_per_cta\": 4, \"ctas_per_sm\": 1, \"pace\": %d", pace);
-        run("g1_persistent", prm, [&] { g1_persistent<8><<<sms, 128>>>(out, state, n, T, pace); });
-    }
-    // G2 one-shot tiles
-    for (uint32_t L : {64u, 128u, 250u, 500u, 1000u}) {
-        if (L > T) continue;
-        for (int W : {1, 2, 4}) {
-            for (int barrier = 0; barrier < 2; ++barrier) {
-                for (int pace : {0, 4}) {
-                    const uint64_t ctas = n / (W * 32 * 8);
-                    snprintf(prm, sizeof prm, "\"npt\": 8, \"warps_per_cta\": %d, \"L\": %u, \"barrier\": %d, \"pace\": %d",
-                             W, L, barrier, pace);
-                    run("g2_tile", prm, [&] {
-                        for (uint32_t k0 = 0; k0 < T; k0 += L) {
-                            const uint32_t l = T - k0 < L ? T - k0 : L;
-                            if (barrier)
-                                g2_tile<8, true><<<(unsigned)ctas, 32 * W>>>(out, state, n, k0, l, pace);
-                            else
-                                g2_tile<8, false><<<(unsigned)ctas, 32 * W>>>(out, state, n, k0, l, pace);
-                        }
-                    });
-                }
-            }
+    // G3 blocked layout
+    for (int W : {1, 4, 8}) {
+        const uint64_t nblk = n / (W * 32 * 8);
+        for (int cps : {1, 2, 4, 16, 0}) {  // 0: one-shot (grid = nblk)
+            const unsigned grid = cps ? sms * cps : (unsigned)nblk;
+            snprintf(prm, sizeof prm, "\"npt\": 8, \"warps_per_cta\": %d, \"ctas_per_sm\": %d", W, cps);
+            run("g3_blocked", prm, [&] { g3_blocked<8><<<grid, 32 * W>>>(out, state, n, T); });
         }
     }
+    // G1 persistent reference
+    snprintf(prm, sizeof prm, "\"npt\": 8, \"warps_per_cta\": 4, \"ctas_per_sm\": 1, \"pace\": 0");
+    run("g1_persistent", prm, [&] { g1_persistent<8><<<sms, 128>>>(out, state, n, T, 0); });
     return 0;
 }
