@@ -524,15 +524,18 @@ def run_ours(a, D):
     if not a.no_probes:
         # the host link with every rank copying at once (barrier-synchronised, sustained):
         # the e2e roofline's denominator, per rank and in aggregate
-        D.barrier()
-        link = P.prng_probe_d2h_sustained_gbs(1 << 30, 8)
+        # (best of 3 barrier-synchronised rounds: a single round is occasionally disturbed)
+        link = 0.0
+        for _ in range(3):
+            D.barrier()
+            link = max(link, P.prng_probe_d2h_sustained_gbs(1 << 30, 8))
         D.barrier()
         per_rank = D.gather(link)
         probes = {"d2h_pinned_concurrent_gbs_per_rank": per_rank,
                   "d2h_pinned_concurrent_gbs_aggregate": sum(per_rank)}
         if D.rank == 0:
             probes.update({"memset_write_gbs": P.prng_probe_memset_gbs(32 << 30, 3),
-                           "fill_kernel_write_gbs": P.prng_probe_fill_gbs(32 << 30, 3),
+                           "fill_kernel_write_gbs": P.prng_probe_fill_gbs(32 << 30, 5),
                            "store_kernel_write_gbs": P.prng_probe_store_gbs(32 << 30, 3),
                            "d2h_pinned_alone_gbs": P.prng_probe_d2h_gbs(1 << 30, 5, True, 1)})
             roofline["frac_of_same_box_memset"] = achieved / probes["memset_write_gbs"]
@@ -545,7 +548,7 @@ def run_ours(a, D):
                     "unit": "GB/s", "frac": agg_gbs / probes["d2h_pinned_concurrent_gbs_aggregate"],
                     "per_rank_frac_min": min(e2e["d2h_gbs_per_gpu_min"] / x for x in per_rank),
                     "peak_source": f"all {D.world} rank(s) at once: pinned cudaMemcpyAsync D2H, 8 x 1 GiB back to "
-                                   f"back per rank after a barrier, summed over ranks"}
+                                   f"back per rank after a barrier (best of 3 rounds), summed over ranks"}
 
     cpu = None
     if D.rank == 0 and D.world == 1 and not a.no_cpu:
