@@ -116,7 +116,7 @@ def parse():
                     help="total numrn per iteration (0 = the BASELINE config: 2^24 at N = 1, 2^28 at N > 1)")
     ap.add_argument("--numiter", type=int, default=0, help="device-only numiter (0 = 1000)")
     ap.add_argument("--e2e-numiter", type=int, default=0, help="end-to-end numiter (0 = 1000 at N = 1, 100 at N > 1)")
-    ap.add_argument("--sustained-steps", type=int, default=100,
+    ap.add_argument("--sustained-steps", type=int, default=200,
                     help="device-only steps of the sustained (power-capped) figure after the timed region; 0 = off")
     ap.add_argument("--seed", type=int, default=SEED_PERF)
     ap.add_argument("--kernel", type=int, default=0, help="kernel variant id (default 0 = auto: v4n8s1 at the bench shape; -1: prng_autotune)")

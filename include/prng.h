@@ -188,7 +188,7 @@ enum prng_option {
                                   0 (default) round-robin, adjacent CTAs hold adjacent
                                   pieces; 1 CTA-blocked, CTA b holds a contiguous run of
                                   units, so concurrently written 4 KiB chunks are spread
-                                  over the whole slot.  Not for cluster variants.          */
+                                  over the whole slot.                                      */
     PRNG_OPT_EPOCH_ITERS = 16  /* epoch-major order for CTA-synchronised variants (output
                                   unchanged): every warp runs each of its pieces through E
                                   iterations, then the next piece; the state goes through
