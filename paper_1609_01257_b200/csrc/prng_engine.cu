@@ -185,6 +185,8 @@ static const char *const kWideNames[] = {"v4n8s1", "v4n16s1", "v2n32s1"};
 // "Default"): v4n8s1 writes 7-9 % faster than v4n4s1 at 2^21..2^24 on some boxes and ties
 // on others; v4n4s1 is ahead at 2^18 and 2^20.
 constexpr uint64_t kAutoWideFrom = 1ull << 21;
+// Shortest time-parallel chunk (iterations); see launch_batch.
+constexpr uint64_t kTpMinChunk = 128;
 
 static int variant_id(const char *name) {
     for (int i = 0; i < kNumVariants; ++i)
@@ -251,21 +253,36 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     const uint64_t piece = 32ull * v.npt;
     a.npieces = (h->count + piece - 1) / piece;
     // Persistent grid: at most one wave of resident warps; equalise pieces per warp.
-    const uint64_t max_warps = max_grid_warps(h, vid, wps);
+    uint64_t max_warps = max_grid_warps(h, vid, wps);
     // Time-parallel mode (NEXT-4): when the pieces cannot fill the grid (small numrn), cut
     // the launch's iterations into chunks started by GF(2) jump-ahead, so that
     // pieces x chunks units fill it.
     uint64_t units = a.npieces;
-    // (chunks >= 256 iterations keep the per-unit 64-step mat-vec below ~10 % of its work)
+    // (chunks >= kTpMinChunk = 128 iterations keep the per-unit 64-step mat-vec -- about 27
+    // iterations' worth of instructions -- near 20 % of its work)
     // Chunks of one piece run concurrently on different warps, so they are only used when
     // the launch does not wrap its slots (iters <= nslots): otherwise two chunks could
     // write the same slot and the earlier iteration could land last.
+    // A time-parallel launch is latency-bound (each warp walks its chunk serially), so it
+    // uses twice the warps per SM of the natural order unless the caller fixed the grid,
+    // and at most one unit per warp: nch = floor(warps / pieces) (measured on the Fig. 4
+    // cells, round 2: 2^12 / 2^14 / 2^16 x 10^4 +39 / +21 / +20 %; raw_r2/m12, m13).
     uint64_t nch = 0;
     if (iters <= nslots) {
-        if (h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters)
+        if (h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters) {
             nch = (iters + h->chunk_iters - 1) / h->chunk_iters;  // PRNG_OPT_CHUNK_ITERS: forced
-        else if (h->time_parallel && 2 * a.npieces <= max_warps && iters >= 512)
-            nch = std::min<uint64_t>((max_warps + a.npieces - 1) / a.npieces, iters / 256);
+        } else if (h->time_parallel && iters >= 2 * kTpMinChunk) {
+            const bool user_grid = h->grid_warps > 0 || h->cta_warps > 0;
+            const uint64_t tp_warps = user_grid ? max_warps : max_grid_warps(h, vid, 2 * v.warps_per_sm);
+            const uint64_t c = std::min<uint64_t>(tp_warps / a.npieces, iters / kTpMinChunk);
+            if (c >= 3) {  // 2 chunks measured no faster than the natural order (2^16: -6 %)
+                nch = c;
+                if (!user_grid) {
+                    wps = 2 * v.warps_per_sm;
+                    max_warps = tp_warps;
+                }
+            }
+        }
     }
     // Anti-absorption, fallback: epoch-major order (batch_kernel_epoch) with E = R, so an
     // address is rewritten only one whole epoch (the full ring) later.
