@@ -160,7 +160,7 @@ enum prng_option {
                                   and without the host syncs mode 1 adds for wall time    */
     PRNG_OPT_KERNEL = 5,       /* kernel variant id (see prng_kernel_variants); 0 = "auto"
                                   (default): v4n8s1a from 2^21 work-items per handle,
-                                  v4n4s1p below, widened / epoch-ordered by the
+                                  v4n4s1p from 2^15, v2n2s1 below, widened / epoch-ordered by the
                                   anti-absorption rule (see PRNG_OPT_EPOCH_ITERS,
                                   prng_last_launch)                                       */
     PRNG_OPT_GRID_WARPS = 6,   /* cap on resident warps of the persistent grid; 0 = auto  */
@@ -223,7 +223,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
  * PRNG_ESTATE otherwise).  best_gbs (may be NULL) gets the winner's probe GB/s. */
 int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err);
 
-/* Number of kernel variants compiled in (8), and the name of one: id 0 "auto" (the
+/* Number of kernel variants compiled in (9), and the name of one: id 0 "auto" (the
  * default, resolved per launch -- see PRNG_OPT_KERNEL); "v<V>n<N>s1" = V-wide u64 vector
  * stores (V = 4: 32 bytes, V = 2: 16 bytes), N numbers per thread, CTA barrier every
  * iteration, 4 warps per SM; suffix "a" = .aligned barrier in uniform rounds, "p" =

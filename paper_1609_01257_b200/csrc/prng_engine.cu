@@ -56,8 +56,9 @@ struct Variant {
 // 6.6-6.9 TB/s with DRAM bytes = algorithmic bytes.
 const Variant kVariants[] = {
     // id 0 "auto" (the default): resolved per launch by launch_batch -- v4n8s1a at >= 2^21
-    // work-items per handle, v4n4s1p below (measured), then widened or run in
-    // epoch order by the anti-absorption rule.  Its own fields (= v4n4s1) size the grid.
+    // work-items per handle, v4n4s1p from 2^15, v2n2s1 below (measured), then
+    // widened or run in epoch order by the anti-absorption rule.  Its own fields (= v4n4s1)
+    // size the grid.
     VAR("auto", 4, 4, false, false),
     // the bench-shape default: one 32-B store per thread per vector, 8 numbers per thread
     // (2 KiB per warp-iteration), .aligned barrier in uniform rounds
@@ -71,6 +72,9 @@ const Variant kVariants[] = {
     VAR("v2n4s1", 2, 4, false, false),
     // one 32-B store per thread, 4 numbers per thread (the round-1 default after v2n4s1)
     VAR("v4n4s1", 4, 4, false, false),
+    // one 16-B store per thread, 2 numbers per thread: 64-gid pieces, so a small handle
+    // spreads over more warps and each warp's iteration is shorter (latency-bound launches)
+    VAR("v2n2s1", 2, 2, false, false),
 };
 #undef VAR
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
@@ -185,6 +189,10 @@ static const char *const kWideNames[] = {"v4n8s1", "v4n16s1", "v2n32s1"};
 // "Default"): v4n8s1 writes 7-9 % faster than v4n4s1 at 2^21..2^24 on some boxes and ties
 // on others; v4n4s1 is ahead at 2^18 and 2^20.
 constexpr uint64_t kAutoWideFrom = 1ull << 21;
+// ... and v2n2s1 (64-gid pieces: more warps for a small handle, shorter iterations per
+// warp) below this many: 5-25 % faster than v4n4s1p from 2^10 to 2^14 work-items at
+// 10^2..10^4 iterations, slower from 2^15 at >= 10^3 (profiles/r2_fig4.md, raw_r2/m17).
+constexpr uint64_t kAutoNarrowBelow = 1ull << 15;
 // Shortest time-parallel chunk (iterations); see launch_batch.
 constexpr uint64_t kTpMinChunk = 128;
 
@@ -200,7 +208,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     int vid = h->kernel;
     int wps = 0;  // warps per SM override (anti-absorption, second choice)
     if (vid == 0) {  // "auto"
-        vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1a" : "v4n4s1p");
+        vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1a" : h->count >= kAutoNarrowBelow ? "v4n4s1p" : "v2n2s1");
         // Anti-absorption, first choice: the narrowest wider variant whose live set exceeds
         // 2x L2 (output identical; measured honest and as fast).  Not with a user grid.
         if (h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 && absorbs(h, vid, nslots, iters)) {

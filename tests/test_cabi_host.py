@@ -76,7 +76,7 @@ def test_null_handle_calls_fail_cleanly():
 def test_variants_named():
     n = P.prng_kernel_variants()
     names = [P.prng_kernel_variant_name(i) for i in range(n)]
-    assert names == ["auto", "v4n8s1a", "v4n4s1p", "v4n8s1", "v4n16s1", "v2n32s1", "v2n4s1", "v4n4s1"]
+    assert names == ["auto", "v4n8s1a", "v4n4s1p", "v4n8s1", "v4n16s1", "v2n32s1", "v2n4s1", "v4n4s1", "v2n2s1"]
     assert n <= 12  # the product library carries no experiment variants
     assert P.prng_kernel_variant_name(n) is None
     assert [P.prng_event_name(i) for i in range(4)] == list(P.EV_NAMES)

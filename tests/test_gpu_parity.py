@@ -11,7 +11,7 @@ from workloads import RAGGED_N, SEED_PARITY, SPEC_GRID_I, SPEC_GRID_N, sample_po
 
 # every kernel variant the library compiles (prng_engine.cu kVariants); each has the NEXT-3
 # scrambled-output and the epoch-order instantiations
-ALL_NAMES = ("auto", "v4n8s1a", "v4n4s1p", "v4n8s1", "v4n16s1", "v2n32s1", "v2n4s1", "v4n4s1")
+ALL_NAMES = ("auto", "v4n8s1a", "v4n4s1p", "v4n8s1", "v4n16s1", "v2n32s1", "v2n4s1", "v4n4s1", "v2n2s1")
 STAR_NAMES = ALL_NAMES[1:]
 
 
@@ -514,9 +514,9 @@ def test_anti_absorption_rule(n, i, R, epoch_opt, expect, out_kind):
 
 
 @pytest.mark.parametrize("n,name", [(1 << 24, "v4n8s1a"), ((1 << 21) - 1, "v4n4s1p"), (1 << 21, "v4n8s1a"),
-                                    ((1 << 21) + 300, "v4n8s1a")])
+                                    ((1 << 21) + 300, "v4n8s1a"), (1 << 15, "v4n4s1p"), ((1 << 15) - 1, "v2n2s1")])
 def test_auto_kernel_at_bench_shape(n, name):
-    """"auto" (id 0): v4n8s1a from 2^21 work-items, v4n4s1p below.  At the bench shape
+    """"auto" (id 0): v4n8s1a from 2^21 work-items, v4n4s1p from 2^15, v2n2s1 below.  At the bench shape
     (2^24 x 1000, default 64 GiB ring = 512 slots) the live set is 512 x 592 x 2 KiB =
     620 MB > 2 x L2, so v4n8s1 runs in natural order; the last iteration and the state vs
     the oracle (sampled gids)."""
