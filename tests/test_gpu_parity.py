@@ -552,8 +552,7 @@ def test_forced_chunks_device_only_bench_shape():
         P.prng_init(h)
         P.prng_generate_device(h, i, buf.data_ptr(), n, i, 0)
         torch.cuda.synchronize()
-        w = _weights(0, n)
-        got = [_gpu_folds(buf[k], w) for k in range(i)]
+        got = [_gpu_folds(buf[k], 0) for k in range(i)]
         last = buf[-1].cpu().numpy().view(np.uint64)
         st = P.prng_read_state(h, n)
     finally:
@@ -918,23 +917,24 @@ def test_randomised_configurations():
 M64 = (1 << 64) - 1
 
 
-def _oracle_folds_threads(n, i, seed, gid_begin=0, count=None, last=False, nthreads=None):
-    """oracle.folds on contiguous gid shards of [gid_begin, gid_begin + count) in parallel
-    threads (ctypes releases the GIL).  The folds combine across shards: XOR, wrapping sum,
-    and the gid-weighted sum (its weights use the global gid); `last` concatenates."""
+def _oracle_folds_threads(n, i, seed, gid_begin=0, count=None, last=False, nthreads=None, shard=1 << 26):
+    """oracle.folds on contiguous gid shards of [gid_begin, gid_begin + count) (at most
+    `shard` gids each, so host memory stays bounded) over a pool of threads (ctypes releases
+    the GIL).  The folds combine across shards: XOR, wrapping sum, and the gid-weighted sum
+    (its weights use the global gid); `last` concatenates."""
     import os
-    import threading
+    from concurrent.futures import ThreadPoolExecutor
     count = n - gid_begin if count is None else count
     nthreads = nthreads or max(1, len(os.sched_getaffinity(0)))
-    res = [None] * nthreads
+    nshards = max(nthreads, (count + shard - 1) // shard)
+    spans = [shard_range(count, r, nshards) for r in range(nshards)]
 
-    def work(r):
-        b, c = shard_range(count, r, nthreads)
-        res[r] = oracle.folds(n, i, seed, gid_begin=gid_begin + b, count=c, last=last) if c else None
+    def work(span):
+        b, c = span
+        return oracle.folds(n, i, seed, gid_begin=gid_begin + b, count=c, last=last) if c else None
 
-    th = [threading.Thread(target=work, args=(r,)) for r in range(nthreads)]
-    [t.start() for t in th]
-    [t.join() for t in th]
+    with ThreadPoolExecutor(nthreads) as ex:
+        res = list(ex.map(work, spans))
     out = {"xor": np.zeros(i, np.uint64), "sum": np.zeros(i, np.uint64), "wsum": np.zeros(i, np.uint64)}
     for rr in res:
         if rr is not None:
@@ -946,23 +946,27 @@ def _oracle_folds_threads(n, i, seed, gid_begin=0, count=None, last=False, nthre
     return out
 
 
-def _gpu_folds(row, weights):
-    """(xor, sum, gid-weighted sum) of one int64 CUDA row; torch's int64 arithmetic wraps
-    mod 2^64 (two's complement), which is the oracle's u64 arithmetic."""
-    s = int(row.sum().item()) & M64
-    w = int((row * weights).sum().item()) & M64
-    v = row.clone()
-    m = v.numel()
-    while m > 1:
-        h2 = m // 2
-        v[:h2] ^= v[m - h2:m]
-        m -= h2
-    return int(v[0].item()) & M64, s, w
-
-
-def _weights(gid_begin, count):
+def _gpu_folds(row, gid0, chunk=1 << 27):
+    """(xor, sum, gid-weighted sum) of one int64 CUDA row whose element j is gid gid0 + j,
+    folded chunk by chunk (bounded temporaries); torch's int64 arithmetic wraps mod 2^64
+    (two's complement), which is the oracle's u64 arithmetic."""
     import torch
-    return torch.arange(count, dtype=torch.int64, device="cuda") * 2 + (2 * gid_begin + 1)
+    x = s = w = 0
+    for c0 in range(0, row.numel(), chunk):
+        part = row[c0:c0 + chunk]
+        wt = torch.arange(part.numel(), dtype=torch.int64, device=part.device) * 2 + (2 * (gid0 + c0) + 1)
+        s += int(part.sum().item())
+        w += int((part * wt).sum().item())
+        del wt
+        v = part.clone()
+        m = v.numel()
+        while m > 1:
+            h2 = m // 2
+            v[:h2] ^= v[m - h2:m]
+            m -= h2
+        x ^= int(v[0].item()) & M64
+        del v
+    return x & M64, s & M64, w & M64
 
 
 def _device_only_full_shape(numrn_total, gid_begin, count, numiter, seed, expect_kernel=None):
@@ -982,11 +986,10 @@ def _device_only_full_shape(numrn_total, gid_begin, count, numiter, seed, expect
         base, pitch, slots, first, end = P.prng_device_ring(h)
         assert end == numiter
         ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
-        w = _weights(gid_begin, count)
-        got = {k: _gpu_folds(ring[(first + k) % slots, :count], w) for k in range(max(0, numiter - slots), numiter)}
+        got = {k: _gpu_folds(ring[(first + k) % slots, :count], gid_begin) for k in range(max(0, numiter - slots), numiter)}
         last = ring[(first + numiter - 1) % slots, :count].cpu().numpy().view(np.uint64).copy()
         st = P.prng_read_state(h)
-        del ring, w
+        del ring
     finally:
         P.prng_destroy(h)
     want = _oracle_folds_threads(numrn_total, numiter, seed, gid_begin, count, last=True)
@@ -1080,8 +1083,7 @@ def test_config2_every_iteration_no_ring():
         P.prng_init(h)
         P.prng_generate_device(h, i, buf.data_ptr(), n, i, torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
-        w = _weights(0, n)
-        got = [_gpu_folds(buf[k], w) for k in range(i)]
+        got = [_gpu_folds(buf[k], 0) for k in range(i)]
     finally:
         P.prng_destroy(h)
     del buf
@@ -1213,3 +1215,38 @@ def test_binding_checks_host_buffer_sizes():
         assert np.array_equal(arr, oracle.stream(n, 2, 0))
     finally:
         P.prng_destroy(h)
+
+
+@pytest.mark.slow
+def test_maximum_numrn_full_range():
+    """The maximum size (A12: numrn = 2^32, every gid of the cl_uint range): one
+    handle over all 2^32 work-items, 3 iterations device-only (a 3-slot ring of 32 GiB slots),
+    every slot's XOR / sum / gid-weighted sum folded on the GPU vs the oracle (all 2^32 gids,
+    sharded so host memory stays bounded), plus sampled gids (the top gid included) and the
+    A3 gid vs the random-access form."""
+    import torch
+    n, i = 1 << 32, 3
+    free, _ = torch.cuda.mem_get_info()
+    if free < (4 * 8 << 32) + (8 << 30):
+        pytest.skip("needs ~136 GB of free device memory")
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, i)
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        base, pitch, slots, first, end = P.prng_device_ring(h)
+        assert (slots, end) == (i, i)
+        ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
+        got = [_gpu_folds(ring[(first + k) % slots, :n], 0) for k in range(i)]
+        g = [0, 1, A3_GID, n - 2, n - 1] + [int(x) for x in np.random.default_rng(4).integers(0, n, 200)]
+        idx = torch.tensor(g, dtype=torch.int64, device="cuda")
+        rows = [ring[(first + k) % slots].index_select(0, idx).cpu().numpy().view(np.uint64) for k in range(i)]
+        del ring
+    finally:
+        P.prng_destroy(h)
+    for k in range(i):
+        for j, gg in enumerate(g):
+            assert int(rows[k][j]) == oracle.sample(gg, k, SEED_PARITY), (k, gg)
+    want = _oracle_folds_threads(n, i, SEED_PARITY)
+    for k in range(i):
+        assert got[k] == (int(want["xor"][k]), int(want["sum"][k]), int(want["wsum"][k])), k
