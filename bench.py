@@ -130,6 +130,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--output", type=int, default=0, help="0 = the state (paper); 1 = xorshift64* scrambled (NEXT-3)")
     ap.add_argument("--no-numa-bind", action="store_true", help="keep the process's CPU affinity")
+    ap.add_argument("--plan", action="store_true",
+                    help="print the multi-rank plan (workloads, every rank's gid range) and exit; no GPU needed")
     ap.add_argument("--device-mod", type=int, default=0,
                     help="TEST ONLY: map local rank r to GPU r %% K (several ranks per GPU; timings meaningless)")
     return ap.parse_args()
@@ -581,16 +583,37 @@ def run_ours(a, D):
         print(json.dumps(line), flush=True)
 
 
+def run_plan(a, D):
+    """--plan: what each rank would run, gathered over the process group (barrier + one-hot
+    SUM, the same collectives as the timed run) and printed by rank 0.  Lets the N > 1 host
+    logic (workload choice, gid sharding, collectives) be checked on CPU with gloo."""
+    W = workload(a.numrn_total, a.numiter, a.e2e_numiter, D.world)
+    gb, cnt = shard_range(W["numrn"], D.rank, D.world)
+    D.barrier()
+    begins, counts = D.gather(float(gb)), D.gather(float(cnt))
+    t = D.max(float(D.rank))
+    if D.rank == 0:
+        print(json.dumps({"plan": True, "n_gpus": D.world, "scaling": W["scaling"],
+                          "config": {"workload": W["workload"], "numrn": W["numrn"], "numiter": W["numiter"],
+                                     "per_gpu": W["per_gpu"], "parallelism": f"gid-shard{D.world}"},
+                          "e2e": {"workload": W["e2e_workload"], "numiter": W["e2e_numiter"],
+                                  "d2h_bytes_per_step": 8 * W["numrn"] * W["e2e_numiter"]},
+                          "ranks": [{"gid_begin": int(b), "count": int(c)} for b, c in zip(begins, counts)],
+                          "max_rank_seen": t}), flush=True)
+
+
 def main():
     a = parse()
-    if a.impl != "reference" and a.dist_backend == "nccl":
+    if a.impl != "reference" and a.dist_backend == "nccl" and not a.plan:
         # bind this rank's GPU before the process group exists (NCCL uses the current device)
         import torch
         local = int(os.environ.get("LOCAL_RANK", "0"))
         torch.cuda.set_device(local % a.device_mod if a.device_mod > 0 else local)
     D = Dist(None if a.impl == "reference" else a.dist_backend)
     try:
-        if a.impl == "reference":
+        if a.plan:
+            run_plan(a, D)
+        elif a.impl == "reference":
             run_reference(a, D)
         else:
             run_ours(a, D)

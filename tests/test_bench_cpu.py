@@ -86,3 +86,28 @@ def test_workload_is_the_baseline_config(world):
         assert "numrn=2^28" in configs[3] and "numiter=100" in configs[4]
     # an explicit off-config shape is labelled as such
     assert not bench.workload(1 << 20, 0, 0, world)["workload"].startswith("BASELINE")
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_plan_under_torchrun_gloo(world):
+    """The driver's N > 1 launch (torchrun, one process per rank) over gloo on CPU with
+    --plan: rank 0 alone prints; the workload is BASELINE config 4 (2^28 total, 2^28 / N per
+    rank) and config 5 for e2e; the ranks' gid ranges (gathered over the process group)
+    are contiguous, disjoint and cover [0, 2^28); the MAX reduction sees every rank."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus",
+                        str(world), "--dist-backend", "gloo", "--plan"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = _lines(r.stdout)
+    assert len(lines) == 1
+    p = lines[0]
+    n = 1 << 28
+    assert p["n_gpus"] == world and p["scaling"] == "strong" and p["max_rank_seen"] == world - 1
+    assert p["config"]["numrn"] == n and p["config"]["per_gpu"] == n // world and p["config"]["numiter"] == 1000
+    assert p["config"]["workload"].startswith("BASELINE config 4")
+    assert p["e2e"]["workload"].startswith("BASELINE config 5") and p["e2e"]["numiter"] == 100
+    ranks = p["ranks"]
+    assert ranks[0]["gid_begin"] == 0 and sum(x["count"] for x in ranks) == n
+    for x, y in zip(ranks, ranks[1:]):
+        assert x["gid_begin"] + x["count"] == y["gid_begin"] and x["count"] == n // world
