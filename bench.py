@@ -79,7 +79,9 @@ def workload(numrn_total: int, numiter: int, e2e_numiter: int, world: int) -> di
         dev = f"BASELINE config 2: numrn={nstr} ({n}) per iteration x numiter={it}, device-only"
         e2e = (f"BASELINE config 3: numrn={nstr} x numiter={e2e_it}, end to end with double-buffered D2H into "
                f"pinned host memory")
-    if numrn_total and n != (DEF_NUMRN_MULTI if multi else DEF_NUMRN) or numiter and it != DEF_NUMITER:
+    off_numrn = bool(numrn_total) and n != (DEF_NUMRN_MULTI if multi else DEF_NUMRN)
+    off_numiter = bool(numiter) and it != DEF_NUMITER
+    if off_numrn or off_numiter:
         dev = dev.replace("BASELINE config", "off-BASELINE shape (cf. config")
     return {"numrn": n, "numiter": it, "e2e_numiter": e2e_it, "workload": dev, "e2e_workload": e2e,
             # N > 1 splits a fixed 2^28 total (config 4); N = 1 is config 2's one-GPU shape

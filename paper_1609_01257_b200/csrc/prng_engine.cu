@@ -765,8 +765,8 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
 static const struct {
     const char *variant;
     int warps_per_sm;
-} kTuneCandidates[] = {{"v4n8s1a", 4}, {"v4n4s1p", 4}, {"v4n4s1", 4}, {"v2n4s1", 4},
-                       {"v2n4s1", 8},  {"v4n8s1", 4},  {"v4n16s1", 4}, {"v2n32s1", 8}};
+} kTuneCandidates[] = {{"v4n8s1a", 4}, {"v4n4s1p", 4}, {"v4n4s1", 4},  {"v2n4s1", 4}, {"v2n4s1", 8},
+                       {"v4n8s1", 4},  {"v4n16s1", 4}, {"v2n32s1", 8}, {"v2n2s1", 4}};
 
 extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err) {
     if (int rc = check_handle(h, err, false)) return rc;
