@@ -460,6 +460,8 @@ def run_ours(a, D):
                 "traffic": traffic, "kernel": kname,
                 "grid_warps": grid_warps or "variant default", "autotune_probe_gbs": tune_gbs,
                 "algorithmic_bytes_per_launch": algo_bytes, "mean_launch_ms": kmean,
+                "best_launch_ms": min(kern_ms), "median_launch_ms": statistics.median(kern_ms),
+                "achieved_best_launch": algo_bytes / (min(kern_ms) * 1e-3) / 1e9,
                 "kernel_share_of_step": sum(kern_ms) / ms, "init_kernel_mean_ms": statistics.mean(init_ms),
                 "peak_source": peak_src,
                 "frac_of_theoretical_hbm3e": achieved / HBM_THEORETICAL_GBS,
