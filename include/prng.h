@@ -120,8 +120,9 @@ int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, pr
  * iteration t of this call goes to dst + (t mod dst_slots) * dst_pitch (u64 elements).
  * dst must be 32-byte aligned and dst_pitch a multiple of 4 with dst_pitch >= count.
  * Enqueued on `stream` (a cudaStream_t, NULL = the handle's generation stream);
- * asynchronous: returns after enqueueing.  prng_init runs on the handle's generation
- * stream: with a different `stream` the caller orders the two (e.g. an event). */
+ * asynchronous: returns after enqueueing.  prng_init and the other generate calls run on
+ * the handle's generation stream: with a different `stream` the caller orders them against
+ * this call (e.g. an event); calls on one handle must not overlap in time. */
 int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch,
                          uint64_t dst_slots, void *stream, prng_err_t *err);
 

@@ -273,8 +273,8 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // write the same slot and the earlier iteration could land last.
     // A time-parallel launch is latency-bound (each warp walks its chunk serially), so it
     // uses twice the warps per SM of the natural order unless the caller fixed the grid,
-    // and at most one unit per warp: nch = floor(warps / pieces) (measured on the Fig. 4
-    // cells, round 2: 2^12 / 2^14 / 2^16 x 10^4 +39 / +21 / +20 %; raw_r2/m12, m13).
+    // and at most one unit per warp: nch = floor(warps / pieces), used only from 3 chunks
+    // (measured on the Fig. 4 cells, profiles/r2_fig4.md).
     uint64_t nch = 0;
     if (iters <= nslots) {
         if (h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters) {
