@@ -1250,3 +1250,31 @@ def test_maximum_numrn_full_range():
     want = _oracle_folds_threads(n, i, SEED_PARITY)
     for k in range(i):
         assert got[k] == (int(want["xor"][k]), int(want["sum"][k]), int(want["wsum"][k])), k
+
+
+def test_order_sensitive_fold_catches_a_misplaced_piece():
+    """Why the full-shape tests fold with sum (2g + 1) x: swap two
+    warp pieces (2 KiB each) of a correct GPU slot -- the XOR and the wrapping sum still
+    match the oracle, the gid-weighted sum does not; a single flipped bit also fails it."""
+    import torch
+    n, i = 1 << 20, 4
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, i)
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        base, pitch, slots, first, _ = P.prng_device_ring(h)
+        ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
+        row = ring[(first + i - 1) % slots, :n].clone()
+    finally:
+        P.prng_destroy(h)
+    want = _oracle_folds_threads(n, i, SEED_PARITY)
+    ok = (int(want["xor"][-1]), int(want["sum"][-1]), int(want["wsum"][-1]))
+    assert _gpu_folds(row, 0) == ok
+    bad = row.clone()
+    bad[1000 * 256:1001 * 256], bad[3000 * 256:3001 * 256] = row[3000 * 256:3001 * 256], row[1000 * 256:1001 * 256]
+    x, s, w = _gpu_folds(bad, 0)
+    assert (x, s) == ok[:2] and w != ok[2]
+    bad = row.clone()
+    bad[12345] ^= 1 << 40
+    assert _gpu_folds(bad, 0)[2] != ok[2]
