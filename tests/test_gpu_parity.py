@@ -425,9 +425,9 @@ def test_forced_chunks_and_piece_order(kname, chunk, order):
 @pytest.mark.parametrize("kname", STAR_NAMES)
 def test_epoch_order(kname, epoch, out_kind):
     """PRNG_OPT_EPOCH_ITERS (epoch-major order: each warp runs its pieces E iterations at a
-    time, the state through HBM between epochs, next unit's state prefetched): every
+    time, the state through HBM between epochs): every
     output of every iteration, split calls, both output transforms, the final state; ragged
-    numrn over several pieces per warp, and numrn with one piece per warp (no prefetch)."""
+    numrn over several pieces per warp, and numrn with one piece per warp."""
     for n, warps in ((70001, 96), (5000, 64)):
         i = 777
         want = (oracle.stream_star if out_kind else oracle.stream)(n, i, SEED_PARITY)
