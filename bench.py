@@ -81,8 +81,11 @@ def workload(numrn_total: int, numiter: int, e2e_numiter: int, world: int) -> di
                f"pinned host memory")
     off_numrn = bool(numrn_total) and n != (DEF_NUMRN_MULTI if multi else DEF_NUMRN)
     off_numiter = bool(numiter) and it != DEF_NUMITER
+    off_e2e = bool(e2e_numiter) and e2e_it != (DEF_NUMITER_C5 if multi else it)
     if off_numrn or off_numiter:
         dev = dev.replace("BASELINE config", "off-BASELINE shape (cf. config")
+    if off_numrn or off_e2e:
+        e2e = e2e.replace("BASELINE config", "off-BASELINE shape (cf. config")
     return {"numrn": n, "numiter": it, "e2e_numiter": e2e_it, "workload": dev, "e2e_workload": e2e,
             # N > 1 splits a fixed 2^28 total (config 4); N = 1 is config 2's one-GPU shape
             "scaling": "strong", "per_gpu": per}

@@ -85,7 +85,9 @@ def test_workload_is_the_baseline_config(world):
         assert W["e2e_workload"].startswith("BASELINE config 5") and "numiter=100" in W["e2e_workload"]
         assert "numrn=2^28" in configs[3] and "numiter=100" in configs[4]
     # an explicit off-config shape is labelled as such
-    assert not bench.workload(1 << 20, 0, 0, world)["workload"].startswith("BASELINE")
+    off = bench.workload(1 << 20, 0, 0, world)
+    assert not off["workload"].startswith("BASELINE") and not off["e2e_workload"].startswith("BASELINE")
+    assert not bench.workload(0, 0, 7, world)["e2e_workload"].startswith("BASELINE")
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
