@@ -191,6 +191,19 @@ class Dist:
             self.dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- NVML handle of a CUDA device
+def nvml_handle(N, dev):
+    """The NVML handle of CUDA device `dev`, matched by PCI bus id (NVML's index order need
+    not be CUDA's), else by index."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(dev)
+        bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+        return N.nvmlDeviceGetHandleByPciBusId(bus)
+    except Exception:  # noqa: BLE001
+        return N.nvmlDeviceGetHandleByIndex(dev)
+
+
 # ---------------------------------------------------------------- clocks during timing
 class Clocks:
     """SM clock + clock-event reasons sampled every 5 ms by NVML (nvidia_ml_py) in a thread
@@ -209,7 +222,7 @@ class Clocks:
             import pynvml as N
             N.nvmlInit()
             self.N = N
-            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.h = nvml_handle(N, self.index)
             self.max = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
             self.rows.append(self._sample())
             self.t = threading.Thread(target=self._loop, daemon=True)
@@ -257,7 +270,7 @@ def bind_to_gpu_cpus(dev):
     try:
         import pynvml as N
         N.nvmlInit()
-        hd = N.nvmlDeviceGetHandleByIndex(dev)
+        hd = nvml_handle(N, dev)
         ncpu = os.cpu_count() or 1
         words = N.nvmlDeviceGetCpuAffinity(hd, (ncpu + 63) // 64)
         cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}

@@ -52,6 +52,8 @@ def test_bench_line_contract():
     e = b["e2e"]
     assert e["d2h_bytes_per_step"] == 8 * (1 << 22) * 200 and e["h2d_bytes_per_step"] == 0 and e["value"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(b["clocks"])
+    assert b["clocks"]["sm_mhz"] and b["clocks"]["sm_max_mhz"]   # NVML found this CUDA device (by PCI bus id)
+    assert "cpus" in (b["config"]["numa_bind"] or {}), b["config"]["numa_bind"]
 
 
 def test_bench_two_ranks_share_one_gpu():
