@@ -25,6 +25,9 @@ cases = [  # (n, iters, variant, mode, output, device-ring slots, PRNG_OPT_EPOCH
     (1 << 20, 70, "auto", P.PRNG_MODE_OVERLAP2, 0, 64, 0),    # anti-absorption: v2n32s1
     (300000, 9, "v4n8s1a", P.PRNG_MODE_OVERLAP2, 0, 16, 0),   # .aligned barrier in uniform rounds
     (300000, 9, "v4n16s1", P.PRNG_MODE_OVERLAP2, 1, 16, 0),   # wide pieces, ragged last piece
+    (3000, 9, "auto", P.PRNG_MODE_OVERLAP2, 0, 16, 0),        # auto -> v2n2s1 (small handle), ragged
+    (4100, 700, "auto", P.PRNG_MODE_OVERLAP2, 1, 1000, 0),    # time-parallel at 8 warps/SM, v2n2s1, star
+    (20000, 300, "v4n4s1p", P.PRNG_MODE_ZEROCOPY, 0, 300, 0), # time-parallel from 256 iterations, O3
 ]
 bad = 0
 for n, it, v, mode, out, slots, epoch in cases:
