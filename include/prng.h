@@ -132,7 +132,10 @@ int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t ds
  * iteration k of this call goes to dst[(k mod dst_rows) * dst_pitch + j], j < count.  For
  * one array shared by all ranks of a node, pass dst = array + gid_begin and dst_pitch =
  * numrn_total.  dst need not be pinned (it is cudaHostRegister'ed for the call if it is
- * not).  Blocks until the copies are done; the array is the caller's. */
+ * not).  Blocks until the copies are done; the array is the caller's.  Every CUDA call is
+ * checked: on a failure the call returns PRNG_ECUDA and the handle is poisoned until
+ * prng_init (tests inject one with the environment variable PRNG_B200_FAULT_AFTER=N, read at
+ * create time: the N-th checked call fails; not for production use). */
 int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch,
                        uint64_t dst_rows, prng_err_t *err);
 
@@ -175,7 +178,10 @@ enum prng_option {
                                   scrambler, A19).  Every kernel variant supports both.    */
     PRNG_OPT_TIME_PARALLEL = 11, /* 1 (default): when numrn is too small to fill the GPU, cut
                                   a launch's iterations into chunks started by GF(2)
-                                  jump-ahead (xs^k is linear: a 64x64 bit matrix); 0: off */
+                                  jump-ahead (xs^k is linear: a 64x64 bit matrix), at 8
+                                  warps per SM, one chunk per warp, >= 3 chunks of >= 128
+                                  iterations, in launches that do not wrap their slots;
+                                  0: off.  Output unchanged.                              */
     PRNG_OPT_BLOCKING = 12,    /* 1 (default): device-only prng_generate returns when the work
                                   is done; 0: returns after enqueueing on the generation
                                   stream (synchronise the stream before reading results)   */
