@@ -1278,3 +1278,68 @@ def test_order_sensitive_fold_catches_a_misplaced_piece():
     bad = row.clone()
     bad[12345] ^= 1 << 40
     assert _gpu_folds(bad, 0)[2] != ok[2]
+
+
+def test_randomised_api_sequences():
+    """Seeded fuzz over sequences of C-ABI calls on one handle: prng_init / prng_seek, then a
+    random mix of prng_generate (sink or device-only ring), prng_generate_device (into a
+    torch buffer, random pitch and slot count) and prng_generate_host (random row ring),
+    with random variant / output / time-parallel options; after every call the emitted
+    iterations (and the state) are compared with the oracle's stream at those positions."""
+    import torch
+    r = np.random.default_rng(777)
+    names = [P.prng_kernel_variant_name(k) for k in range(P.prng_kernel_variants())]
+    for trial in range(40):
+        n = int(r.choice([1, 5, 64, 129, 1000, 4099, 30001]))
+        seed = int(r.integers(0, 1 << 63))
+        star = int(r.random() < 0.3)
+        start = int(r.choice([0, 0, 1, 7, 300]))
+        total = start + 700
+        want = (oracle.stream_star if star else oracle.stream)(n, total, seed)
+        plain = oracle.stream(n, total, seed)
+        h = P.prng_create(n, seed)
+        try:
+            P.prng_set_option(h, P.PRNG_OPT_KERNEL, int(r.integers(0, len(names))))
+            P.prng_set_option(h, P.PRNG_OPT_OUTPUT, star)
+            P.prng_set_option(h, P.PRNG_OPT_TIME_PARALLEL, int(r.random() < 0.8))
+            P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, int(r.choice([0, 1, 3, 64])))
+            if start:
+                P.prng_seek(h, start)
+            else:
+                P.prng_init(h)
+            pos = start
+            while pos < total:
+                m = int(min(total - pos, r.choice([1, 2, 9, 130, 300])))
+                kind = int(r.integers(0, 4))
+                ctx = dict(trial=trial, n=n, pos=pos, m=m, kind=kind, star=star)
+                if kind == 0:    # end to end through the copy sink
+                    out = np.zeros((m, n), np.uint64)
+                    P.prng_generate(h, m, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, pos, m, 0))
+                    assert np.array_equal(out, want[pos:pos + m]), ctx
+                elif kind == 1:  # device only through the handle's ring
+                    slots = int(r.choice([1, 3, 1000]))
+                    P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, slots)
+                    P.prng_generate(h, m)
+                    _, _, R, first, end = P.prng_device_ring(h)
+                    assert end == pos + m, ctx
+                    for k in range(max(pos, pos + m - R), pos + m):
+                        assert np.array_equal(P.prng_read_slot(h, (first + k) % R), want[k]), (ctx, k)
+                elif kind == 2:  # device only into a caller-owned torch buffer
+                    pitch = (n + 3) // 4 * 4 + 4 * int(r.integers(0, 3))
+                    dslots = int(r.choice([m, max(1, m // 2), 1]))
+                    buf = torch.zeros((dslots, pitch), dtype=torch.int64, device="cuda")
+                    P.prng_generate_device(h, m, buf.data_ptr(), pitch, dslots, 0)
+                    torch.cuda.synchronize()
+                    got = buf[:, :n].cpu().numpy().view(np.uint64)
+                    for t in range(max(0, m - dslots), m):
+                        assert np.array_equal(got[t % dslots], want[pos + t]), (ctx, t)
+                else:            # end to end straight into a host array (row ring)
+                    rows = int(r.choice([m, 2, 1]))
+                    arr = np.zeros((rows, n), np.uint64)
+                    P.prng_generate_host(h, m, arr, n, rows)
+                    for t in range(max(0, m - rows), m):
+                        assert np.array_equal(arr[t % rows], want[pos + t]), (ctx, t)
+                pos += m
+                assert np.array_equal(P.prng_read_state(h), plain[pos - 1]), ctx
+        finally:
+            P.prng_destroy(h)
