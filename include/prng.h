@@ -95,7 +95,9 @@ void prng_destroy(prng_t *h);
 int prng_set_streams(prng_t *h, void *gen_stream, void *copy_stream, prng_err_t *err);
 
 /* a1 -- the init kernel: state[g] = seed64(g, seed) on the device; the stream
- * position is reset to iteration 0 (the next iteration emitted is the seeds themselves). */
+ * position is reset to iteration 0 (the next iteration emitted is the seeds themselves).
+ * With PRNG_OPT_FUSED_SEED 1 (the default) no kernel runs here: the next batch launch
+ * computes the seeds in registers (same output). */
 int prng_init(prng_t *h, prng_err_t *err);
 
 /* Checkpoint / resume: re-seed (as prng_init) and position the stream so that the next
@@ -122,7 +124,9 @@ int prng_generate(prng_t *h, uint64_t numiter, prng_sink_fn sink, void *user, pr
  * Enqueued on `stream` (a cudaStream_t, NULL = the handle's generation stream);
  * asynchronous: returns after enqueueing.  prng_init and the other generate calls run on
  * the handle's generation stream: with a different `stream` the caller orders them against
- * this call (e.g. an event); calls on one handle must not overlap in time. */
+ * this call (e.g. an event); calls on one handle must not overlap in time.  (With
+ * PRNG_OPT_FUSED_SEED 1, prng_init enqueues nothing: the seeds are computed by this call's
+ * own kernel on `stream`.) */
 int prng_generate_device(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_pitch,
                          uint64_t dst_slots, void *stream, prng_err_t *err);
 
@@ -179,7 +183,7 @@ enum prng_option {
     PRNG_OPT_TIME_PARALLEL = 11, /* 1 (default): when numrn is too small to fill the GPU, cut
                                   a launch's iterations into chunks started by GF(2)
                                   jump-ahead (xs^k is linear: a 64x64 bit matrix), at 8
-                                  warps per SM, one chunk per warp, >= 3 chunks of >= 128
+                                  warps per SM, one chunk per warp, >= 3 chunks of >= 48 
                                   iterations, in launches that do not wrap their slots;
                                   0: off.  Output unchanged.                              */
     PRNG_OPT_BLOCKING = 12,    /* 1 (default): device-only prng_generate returns when the work
@@ -196,7 +200,7 @@ enum prng_option {
                                   pieces; 1 CTA-blocked, CTA b holds a contiguous run of
                                   units, so concurrently written 4 KiB chunks are spread
                                   over the whole slot.                                      */
-    PRNG_OPT_EPOCH_ITERS = 16  /* epoch-major order for CTA-synchronised variants (output
+    PRNG_OPT_EPOCH_ITERS = 16, /* epoch-major order for CTA-synchronised variants (output
                                   unchanged): every warp runs each of its pieces through E
                                   iterations, then the next piece; the state goes through
                                   HBM between epochs (+16 B per number per epoch).
@@ -205,6 +209,15 @@ enum prng_option {
                                   bytes per warp-iteration) are < 2x L2, so no address is
                                   rewritten while its line may still be in L2 (DESIGN.md
                                   §5); E > 0 forced; -1 off.                                */
+    PRNG_OPT_FUSED_SEED = 17   /* 1 (default): prng_init only records that the stream restarts;
+                                  the next batch launch computes the seeds (a1) in registers
+                                  before its first iteration -- one launch and 16 B per
+                                  work-item of state traffic less, output unchanged.  Calls
+                                  that read the state array directly (prng_read_state,
+                                  prng_seek) run the seed kernel first.  0: prng_init
+                                  launches the seed kernel itself (the paper's separate
+                                  `init` kernel; its interval is INIT_KERNEL in the
+                                  profile, as in Fig. 5).                                   */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two

@@ -25,7 +25,7 @@ __all__ = [
     "CopySink", "DigestSink", "SINK_FN",
     "PRNG_OPT_MODE", "PRNG_OPT_BATCH_ITERS", "PRNG_OPT_RING_SLOTS", "PRNG_OPT_PROFILE",
     "PRNG_OPT_KERNEL", "PRNG_OPT_GRID_WARPS", "PRNG_OPT_RING_PAD", "PRNG_OPT_HOST_MEM", "PRNG_OPT_CHUNK_ITERS",
-    "PRNG_OPT_PIECE_ORDER", "PRNG_OPT_EPOCH_ITERS", "PRNG_MODE_ZEROCOPY", "PRNG_MODE_SERIAL", "PRNG_MODE_PAGEABLE",
+    "PRNG_OPT_PIECE_ORDER", "PRNG_OPT_EPOCH_ITERS", "PRNG_OPT_FUSED_SEED", "PRNG_MODE_ZEROCOPY", "PRNG_MODE_SERIAL", "PRNG_MODE_PAGEABLE",
     "PRNG_MODE_OVERLAP1", "PRNG_MODE_OVERLAP2", "EV_NAMES",
 ]
 
@@ -34,7 +34,7 @@ PRNG_OK, PRNG_EINVAL, PRNG_ESTATE, PRNG_ENOMEM, PRNG_ECUDA, PRNG_ESINK = 0, -1, 
 PRNG_OPT_MODE, PRNG_OPT_BATCH_ITERS, PRNG_OPT_RING_SLOTS = 1, 2, 3
 PRNG_OPT_PROFILE, PRNG_OPT_KERNEL, PRNG_OPT_GRID_WARPS, PRNG_OPT_RING_PAD, PRNG_OPT_HOST_MEM = 4, 5, 6, 7, 8
 PRNG_OPT_OUTPUT, PRNG_OPT_TIME_PARALLEL, PRNG_OPT_BLOCKING, PRNG_OPT_CTA_WARPS = 10, 11, 12, 13
-PRNG_OPT_CHUNK_ITERS, PRNG_OPT_PIECE_ORDER, PRNG_OPT_EPOCH_ITERS = 14, 15, 16
+PRNG_OPT_CHUNK_ITERS, PRNG_OPT_PIECE_ORDER, PRNG_OPT_EPOCH_ITERS, PRNG_OPT_FUSED_SEED = 14, 15, 16, 17
 PRNG_MODE_SERIAL, PRNG_MODE_PAGEABLE, PRNG_MODE_OVERLAP1, PRNG_MODE_OVERLAP2, PRNG_MODE_ZEROCOPY = 0, 1, 2, 3, 4
 EV_NAMES = ("INIT_KERNEL", "RNG_KERNEL", "READ_BUFFER", "OUT")
 

@@ -65,6 +65,11 @@ struct prng {
     uint64_t numrn_total = 0, seed = 0, gid_begin = 0, count = 0;
     uint64_t pos = 0;  // iterations emitted since prng_init
     bool inited = false, poisoned = false;
+    // a1 fused (PRNG_OPT_FUSED_SEED): prng_init only marks the seeds pending; the next batch
+    // launch computes them in registers (or materialize_seeds runs seed_kernel first when
+    // something reads d_state directly)
+    bool seed_pending = false;
+    int fused_seed = 1;
 
     uint64_t *d_state = nullptr;   // [round_up(count, 4)]
     uint64_t *d_state2 = nullptr;  // the other half of the state double buffer (time-parallel launches)
@@ -141,6 +146,8 @@ int prof_end(prng *h, cudaStream_t s, prng_err_t *err);
 int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64_t slot0, uint32_t iters,
                  bool first_is_state, cudaStream_t s, prng_err_t *err);
 int check_handle(prng *h, prng_err_t *err, bool need_init);
+// Run the pending a1 (seed_kernel into d_state on s_gen) if prng_init deferred it.
+int materialize_seeds(prng *h, prng_err_t *err);
 // prng_pipeline.cu: the end-to-end modes (S0, S1, O1, O2, O3) of prng_generate with a sink.
 int generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void *user, prng_err_t *err);
 

@@ -193,8 +193,10 @@ constexpr uint64_t kAutoWideFrom = 1ull << 21;
 // warp) below this many: 5-25 % faster than v4n4s1p from 2^10 to 2^14 work-items at
 // 10^2..10^4 iterations, slower from 2^15 at >= 10^3 (profiles/r2_fig4.md, raw_r2/m17).
 constexpr uint64_t kAutoNarrowBelow = 1ull << 15;
-// Shortest time-parallel chunk (iterations); see launch_batch.
-constexpr uint64_t kTpMinChunk = 128;
+// Shortest time-parallel chunk (iterations); see launch_batch.  48 measured at least as fast
+// as 128 / 64 / 32 on the small-n cells and faster from 200 to 1000 iterations at <= 2^13
+// work-items (profiles/r2_fig4.md "Round-2 session 3", raw_r2/m25).
+constexpr uint64_t kTpMinChunk = 48;
 
 static int variant_id(const char *name) {
     for (int i = 0; i < kNumVariants; ++i)
@@ -257,6 +259,9 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     a.jump = nullptr;
     a.state_out = h->d_state;
     a.order = (uint32_t)h->piece_order;
+    a.seeding = h->seed_pending ? 1u : 0u;  // a1 fused: this launch starts from the seeds
+    a.seed = h->seed;
+    a.gid_begin = h->gid_begin;
 
     const uint64_t piece = 32ull * v.npt;
     a.npieces = (h->count + piece - 1) / piece;
@@ -266,8 +271,9 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // the launch's iterations into chunks started by GF(2) jump-ahead, so that
     // pieces x chunks units fill it.
     uint64_t units = a.npieces;
-    // (chunks >= kTpMinChunk = 128 iterations keep the per-unit 64-step mat-vec -- about 27
-    // iterations' worth of instructions -- near 20 % of its work)
+    // (chunks >= kTpMinChunk = 48 iterations: the per-unit 64-step mat-vec costs about 27
+    // iterations' worth of instructions, but such launches are latency-bound, not
+    // issue-bound, so a shorter critical path wins)
     // Chunks of one piece run concurrently on different warps, so they are only used when
     // the launch does not wrap its slots (iters <= nslots): otherwise two chunks could
     // write the same slot and the earlier iteration could land last.
@@ -348,7 +354,27 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     fn<<<(unsigned)blocks, (unsigned)(32 * wpb), 0, s>>>(a);
     if (a.jump) std::swap(h->d_state, h->d_state2);  // time-parallel: the final state is in the other half
     CU(cudaGetLastError());
+    h->seed_pending = false;  // every launch writes the whole state array
     return prof_end(h, s, err);
+}
+
+// a1 as its own kernel (the paper's `init`) into d_state on s_gen.
+static int seed_launch(prng *h, prng_err_t *err) {
+    prngk::SeedArgs a{h->d_state, h->count, h->gid_begin, h->seed};
+    const uint64_t pairs = (h->count + 1) / 2;
+    const uint64_t max_blocks = (uint64_t)h->num_sms * 8;
+    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((pairs + kBlock - 1) / kBlock, max_blocks));
+    if (int rc = prof_begin(h, h->s_gen, PRNG_EV_INIT_KERNEL, err)) return rc;
+    prngk::seed_kernel<<<(unsigned)blocks, kBlock, 0, h->s_gen>>>(a);
+    CU(cudaGetLastError());
+    return prof_end(h, h->s_gen, err);
+}
+
+int materialize_seeds(prng *h, prng_err_t *err) {
+    if (!h->seed_pending) return PRNG_OK;
+    if (int rc = seed_launch(h, err)) return rc;
+    h->seed_pending = false;
+    return PRNG_OK;
 }
 
 int check_handle(prng *h, prng_err_t *err, bool need_init) {
@@ -579,6 +605,10 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             if (value < -1 || value > 0xFFFFFFFFll) return set_err(err, PRNG_EINVAL, "bad epoch iterations");
             h->epoch_iters = value;
             break;
+        case PRNG_OPT_FUSED_SEED:
+            if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad fused-seed flag");
+            h->fused_seed = (int)value;
+            break;
 
 
         default:
@@ -605,6 +635,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_CHUNK_ITERS: *value = h->chunk_iters; break;
         case PRNG_OPT_PIECE_ORDER: *value = h->piece_order; break;
         case PRNG_OPT_EPOCH_ITERS: *value = h->epoch_iters; break;
+        case PRNG_OPT_FUSED_SEED: *value = h->fused_seed; break;
 
 
         default: return set_err(err, PRNG_EINVAL, "unknown option %d", option);
@@ -620,17 +651,15 @@ int prng_init(prng_t *h, prng_err_t *err) {
     if (h->profile != 2) clear_prof(h);  // 2: intervals accumulate across runs
     if (int rc = ensure_origin(h, err)) return rc;
     const double t0 = now_s();
-    prngk::SeedArgs a{h->d_state, h->count, h->gid_begin, h->seed};
-    const uint64_t pairs = (h->count + 1) / 2;
-    const uint64_t max_blocks = (uint64_t)h->num_sms * 8;
-    const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((pairs + kBlock - 1) / kBlock, max_blocks));
-    if (int rc = prof_begin(h, h->s_gen, PRNG_EV_INIT_KERNEL, err)) return rc;
-    prngk::seed_kernel<<<(unsigned)blocks, kBlock, 0, h->s_gen>>>(a);
-    CU(cudaGetLastError());
-    if (int rc = prof_end(h, h->s_gen, err)) return rc;
     h->pos = 0;
     h->ring_iter0 = h->ring_cursor;
     h->inited = true;
+    if (h->fused_seed) {  // a1 runs inside the next batch launch
+        h->seed_pending = true;
+        return ok(err);
+    }
+    h->seed_pending = false;
+    if (int rc = seed_launch(h, err)) return rc;
     if (h->profile == 1) {
         CU(cudaStreamSynchronize(h->s_gen));
         h->wall_s += now_s() - t0;
@@ -647,6 +676,7 @@ int prng_init(prng_t *h, prng_err_t *err) {
 int prng_seek(prng_t *h, uint64_t iteration, prng_err_t *err) {
     if (int rc = prng_init(h, err)) return rc;
     if (iteration == 0) return ok(err);
+    if (int rc = materialize_seeds(h, err)) return rc;  // the jump reads the seeds from d_state
     if (h->jump_cap < 2) {
         if (h->d_jump) cudaFree(h->d_jump);
         h->d_jump = nullptr;
@@ -858,6 +888,7 @@ int prng_read_slot(prng_t *h, uint64_t slot, uint64_t *host_dst, prng_err_t *err
 int prng_read_state(prng_t *h, uint64_t *host_dst, prng_err_t *err) {
     if (int rc = check_handle(h, err, false)) return rc;
     if (!host_dst) return set_err(err, PRNG_EINVAL, "NULL destination");
+    if (int rc = materialize_seeds(h, err)) return rc;
     CU(cudaStreamSynchronize(h->s_gen));
     CU(cudaMemcpy(host_dst, h->d_state, h->count * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     return ok(err);

@@ -107,6 +107,22 @@ __device__ __forceinline__ void load_vec(const uint64_t *p, uint64_t *x) {
         ld_v2(p, x[0], x[1]);
 }
 
+// Weak (non-.nc) loads: the epoch kernel re-reads states that the same thread wrote at the
+// end of its previous unit (see batch_kernel_epoch).
+__device__ __forceinline__ void ld_v4_wk(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
+    asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+__device__ __forceinline__ void ld_v2_wk(const uint64_t *p, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+template <int VEC>
+__device__ __forceinline__ void load_vec_wk(const uint64_t *p, uint64_t *x) {
+    if constexpr (VEC == 4)
+        ld_v4_wk(p, x[0], x[1], x[2], x[3]);
+    else
+        ld_v2_wk(p, x[0], x[1]);
+}
+
 // ---------------------------------------------------------------- a1: seed kernel
 struct SeedArgs {
     uint64_t *state;     // [count] out, 16-byte aligned
@@ -157,7 +173,51 @@ struct BatchArgs {
     uint64_t *state_out;      // nchunks > 1: the last chunk writes the final state here
     uint32_t order;           // 0: unit r*W + w to warp w in round r (adjacent CTAs, adjacent
                               //    pieces); 1: CTA b takes units [b*rounds*wpb, (b+1)*rounds*wpb)
+    // a1 fused into the launch (PRNG_OPT_FUSED_SEED): seeding != 0 -> a unit computes its
+    // start states as seed64(gid_begin + gid, premix64(seed)) in registers instead of
+    // loading them from `state` (which it still writes at the end); the launch then
+    // behaves exactly as if seed_kernel had written `state` before it.
+    uint32_t seeding;
+    uint64_t seed;
+    uint64_t gid_begin;
 };
+
+// The start states of a lane's NPT gids (handle-relative base, VEC-wide groups vs apart):
+// seeds computed in registers (a1 fused) or loaded from the state array.  Gids at or past
+// `count` (the ragged last piece, PARTIAL only) get 0 and are never stored.
+template <int VEC, int NPT, bool FULLP, bool NC = true>
+__device__ __forceinline__ void start_states(const BatchArgs &a, uint64_t base, uint64_t vs, uint64_t *x,
+                                             bool seed_now) {
+    constexpr int NV = NPT / VEC;
+    if (seed_now) {
+        const uint64_t m = premix64(a.seed);
+        const uint32_t key_hi = (uint32_t)m, key_lo = (uint32_t)(m >> 32);
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const uint64_t idx = base + (uint64_t)v * vs + e;
+                const uint64_t s = seed64((uint32_t)(a.gid_begin + idx), key_hi, key_lo);
+                x[v * VEC + e] = (FULLP || idx < a.count) ? s : 0ull;
+            }
+    } else if constexpr (FULLP) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            if constexpr (NC)
+                load_vec<VEC>(a.state + base + (uint64_t)v * vs, x + v * VEC);
+            else
+                load_vec_wk<VEC>(a.state + base + (uint64_t)v * vs, x + v * VEC);
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const uint64_t idx = base + (uint64_t)v * vs + e;
+                x[v * VEC + e] = idx < a.count ? a.state[idx] : 0ull;
+            }
+    }
+}
 
 // y = J x over GF(2): XOR of the columns J e_i selected by the bits of x (xs^k is linear).
 __device__ __forceinline__ uint64_t gf2_matvec(const uint64_t *__restrict__ J, uint64_t x) {
@@ -255,19 +315,8 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
     constexpr uint64_t vs = 32ull * VEC;  // elements between a lane's vectors
     const uint64_t base = u.base;
     uint64_t x[NPT];
-    // ---- load the NPT states of this lane (read once per unit)
-    if constexpr (MODE == FULL) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) load_vec<VEC>(a.state + base + (uint64_t)v * vs, x + v * VEC);
-    } else {
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                const uint64_t idx = base + (uint64_t)v * vs + e;
-                x[v * VEC + e] = idx < a.count ? a.state[idx] : 0ull;
-            }
-    }
+    // ---- the NPT start states of this lane (read once per unit, or seeded: a1 fused)
+    start_states<VEC, NPT, MODE == FULL>(a, base, vs, x, a.seeding != 0);
     if (u.jump) {  // time-parallel chunk: jump ahead (c*L + e) steps in one GF(2) mat-vec
 #pragma unroll
         for (int j = 0; j < NPT; ++j) x[j] = gf2_matvec(u.jump, x[j]);
@@ -436,20 +485,6 @@ __global__ void __launch_bounds__(256) batch_kernel(BatchArgs a) {
 // program order, PTX memory model) -- and measured faster than a .cg (LDG.STRONG.GPU)
 // load or prefetching the next unit's state during the current one (exp21).  CTA barrier
 // every iteration as in batch_kernel.
-__device__ __forceinline__ void ld_v4_wk(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
-    asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
-}
-__device__ __forceinline__ void ld_v2_wk(const uint64_t *p, uint64_t &a, uint64_t &b) {
-    asm volatile("ld.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
-}
-template <int VEC>
-__device__ __forceinline__ void load_vec_wk(const uint64_t *p, uint64_t *x) {
-    if constexpr (VEC == 4)
-        ld_v4_wk(p, x[0], x[1], x[2], x[3]);
-    else
-        ld_v2_wk(p, x[0], x[1]);
-}
-
 // One unit of the epoch kernel: a piece through iterations [t_begin, t_begin + t_count).
 template <int VEC, int NPT, int OUT, bool FULL, bool AL = false>
 __device__ __forceinline__ void epoch_unit(const BatchArgs &a, uint64_t *x, uint64_t base, uint32_t slot,
@@ -525,9 +560,9 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
             const uint64_t piece = r * nwarps + warp;
             const uint64_t base = piece * PIECE + (uint64_t)lane * VEC;
             uint64_t x[NPT];
+            const bool seed_now = e == 0 && a.seeding != 0;  // a1 fused: epoch 0 starts from the seeds
             if ((piece + 1) * PIECE <= a.count) {
-#pragma unroll
-                for (int v = 0; v < NV; ++v) load_vec_wk<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+                start_states<VEC, NPT, true, false>(a, base, 32ull * VEC, x, seed_now);
                 // uniform round: all of the CTA's active warps hold a full piece in round r
                 const uint64_t last = r * nwarps + cta_warp0 + bar_threads / 32 - 1;
                 if (AL && last < a.npieces && (last + 1) * PIECE <= a.count)
@@ -537,13 +572,7 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) store_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
             } else {  // the ragged last piece
-#pragma unroll
-                for (int v = 0; v < NV; ++v)
-#pragma unroll
-                    for (int q = 0; q < VEC; ++q) {
-                        const uint64_t idx = base + (uint64_t)v * 32 * VEC + q;
-                        x[v * VEC + q] = idx < a.count ? a.state[idx] : 0ull;
-                    }
+                start_states<VEC, NPT, false>(a, base, 32ull * VEC, x, seed_now);
                 epoch_unit<VEC, NPT, OUT, false>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
 #pragma unroll
                 for (int v = 0; v < NV; ++v)

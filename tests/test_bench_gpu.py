@@ -44,7 +44,8 @@ def test_bench_line_contract():
               "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert k in b, k
     assert b["metric"] == _metric() and b["n_gpus"] == 1 and b["steps"] == 2 and b["value"] > 0
-    assert b["gpu_launches"] == 2 * b["steps"]  # seed + batch kernel per step
+    # one batch kernel per step: a1 is fused into it (PRNG_OPT_FUSED_SEED default), no seed kernel
+    assert b["gpu_launches"] == b["steps"] and b["roofline"]["init_kernel_mean_ms"] is None
     rf = b["roofline"]
     assert rf["bound"] == "hbm" and rf["achieved"] > 0 and rf["frac"] == pytest.approx(rf["achieved"] / rf["peak"])
     assert rf["algorithmic_bytes_per_launch"] == 8 * (1 << 22) * 200

@@ -30,11 +30,12 @@ def _gpu():
 
 
 def run_e2e(numrn, numiter, seed=0, mode=P.PRNG_MODE_OVERLAP2, batch=0, kernel=0, gid_begin=0, count=None,
-            calls=None, profile=False):
+            calls=None, profile=False, fused=1):
     """Generate through prng_generate with the copy sink; returns [numiter, count] uint64."""
     count = numrn - gid_begin if count is None else count
     h = P.prng_create_range(numrn, seed, gid_begin, count)
     try:
+        P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, fused)
         P.prng_set_option(h, P.PRNG_OPT_MODE, mode)
         P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, batch)
         P.prng_set_option(h, P.PRNG_OPT_KERNEL, kernel)
@@ -243,18 +244,20 @@ def test_python_sink_sees_ordered_batches():
     assert np.array_equal(np.concatenate([s[4] for s in seen]), oracle.stream(333, 7, 5))
 
 
+@pytest.mark.parametrize("fused", [0, 1])
 @pytest.mark.parametrize("mode", [P.PRNG_MODE_OVERLAP1, P.PRNG_MODE_OVERLAP2])
-def test_profile_causality(mode):
+def test_profile_causality(mode, fused):
     """S:501 causality on the recorded intervals: READ_j starts after RNG_j ends; RNG_{j+2}
-    (which overwrites RNG_j's device half) starts after READ_j ends; counts per S:496."""
+    (which overwrites RNG_j's device half) starts after READ_j ends; counts per S:496 (one
+    INIT_KERNEL with the paper's separate init kernel, none when a1 is fused)."""
     n, i, T = 1 << 16, 12, 2
-    out, (ids, s, e, wall) = run_e2e(n, i, 3, mode=mode, batch=T, profile=True)
+    out, (ids, s, e, wall) = run_e2e(n, i, 3, mode=mode, batch=T, profile=True, fused=fused)
     assert np.array_equal(out, oracle.stream(n, i, 3))
     nb = i // T
     rng = [(a, b) for n_, a, b in zip(ids, s, e) if n_ == 1]
     rd = [(a, b) for n_, a, b in zip(ids, s, e) if n_ == 2]
     outs = [(a, b) for n_, a, b in zip(ids, s, e) if n_ == 3]
-    assert (ids == 0).sum() == 1 and len(rng) == nb and len(rd) == nb and len(outs) == nb
+    assert (ids == 0).sum() == 1 - fused and len(rng) == nb and len(rd) == nb and len(outs) == nb
     eps = 2e-6
     for j in range(nb):
         assert rd[j][0] >= rng[j][1] - eps
@@ -347,7 +350,7 @@ def test_star_output_any_variant_any_order():
 
 # ---------------------------------------------------------------- NEXT-4: time-parallel jump-ahead
 @pytest.mark.parametrize("n", [1, 33, 1000, 4099])
-@pytest.mark.parametrize("i", [300, 1001, 2600])
+@pytest.mark.parametrize("i", [150, 300, 1001, 2600])
 def test_time_parallel_device_only(n, i):
     """Small numrn: the launch is cut into iteration chunks started by GF(2) jump-ahead.
     Every output of every iteration vs the oracle, and the final state."""
@@ -639,13 +642,16 @@ def test_time_parallel_star(kname):
     assert np.array_equal(out, oracle.stream_star(n, i, 2))
 
 
-def test_nonblocking_accumulated_profile():
+@pytest.mark.parametrize("fused", [0, 1])
+def test_nonblocking_accumulated_profile(fused):
     """bench.py's timed loop: PRNG_OPT_BLOCKING 0 + PRNG_OPT_PROFILE 2 -- K runs enqueued
-    back to back, intervals accumulated, results identical."""
+    back to back, intervals accumulated, results identical; one launch per run when a1 is
+    fused, two (seed + batch) when not."""
     import torch
     n, i, K = 5000, 40, 3
     h = P.prng_create(n, 8)
     try:
+        P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, fused)
         P.prng_set_option(h, P.PRNG_OPT_PROFILE, 2)
         P.prng_set_option(h, P.PRNG_OPT_BLOCKING, 0)
         for _ in range(K):
@@ -653,7 +659,7 @@ def test_nonblocking_accumulated_profile():
             P.prng_generate(h, i)
         torch.cuda.synchronize()
         ids, s, e, _ = P.prng_prof_events(h)
-        assert (ids == 0).sum() == K and (ids == 1).sum() == K and (e >= s).all()
+        assert (ids == 0).sum() == K * (1 - fused) and (ids == 1).sum() == K and (e >= s).all()
         P.prng_set_option(h, P.PRNG_OPT_BLOCKING, 1)
         assert np.array_equal(P.prng_read_state(h, n), oracle.stream(n, i, 8)[-1])
     finally:
@@ -1343,3 +1349,124 @@ def test_randomised_api_sequences():
                 assert np.array_equal(P.prng_read_state(h), plain[pos - 1]), ctx
         finally:
             P.prng_destroy(h)
+
+
+# ---------------------------------------------------------------- a1 fused into the batch launch
+# PRNG_OPT_FUSED_SEED 1 (default): prng_init enqueues nothing and the next batch kernel
+# computes seed64 in registers (prng_kernels.cuh start_states); 0: the paper's separate
+# seed kernel.  Both must give the oracle's stream on every launch form.
+FUSED_PATHS = ("ring", "time_parallel", "epoch", "chunks", "e2e", "zerocopy", "host", "device_stream")
+
+
+def _run_path(path, kname, fused, output, n, i, seed, gid_begin=0, count=None):
+    import torch
+    count = n - gid_begin if count is None else count
+    h = P.prng_create_range(n, seed, gid_begin, count)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, fused)
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid(kname))
+        P.prng_set_option(h, P.PRNG_OPT_OUTPUT, output)
+        if path == "epoch":
+            P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, 3)
+        if path == "chunks":
+            P.prng_set_option(h, P.PRNG_OPT_CHUNK_ITERS, 4)
+        P.prng_init(h)
+        if path in ("ring", "time_parallel", "epoch", "chunks"):
+            if path != "time_parallel":
+                P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, i)
+            P.prng_generate(h, i)
+            _, _, slots, first, _ = P.prng_device_ring(h)
+            out = np.stack([P.prng_read_slot(h, (first + k) % slots, count) for k in range(i)])
+            vid, ep = P.prng_last_launch(h)
+        elif path in ("e2e", "zerocopy"):
+            P.prng_set_option(h, P.PRNG_OPT_MODE, P.PRNG_MODE_ZEROCOPY if path == "zerocopy" else P.PRNG_MODE_OVERLAP2)
+            P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 3)
+            out = np.zeros((i, count), np.uint64)
+            P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), count, 0, i, gid_begin))
+        elif path == "host":
+            out = np.zeros((i, count), np.uint64)
+            P.prng_generate_host(h, i, out, count, i)
+        else:  # caller-owned device buffer on torch's stream
+            pitch = (count + 3) // 4 * 4
+            buf = torch.zeros((i, pitch), dtype=torch.int64, device="cuda")
+            P.prng_generate_device(h, i, buf.data_ptr(), pitch, i, torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            out = buf[:, :count].cpu().numpy().view(np.uint64).copy()
+        st = P.prng_read_state(h, count)
+    finally:
+        P.prng_destroy(h)
+    return out, st
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("path", FUSED_PATHS)
+@pytest.mark.parametrize("kname", ["auto", "v4n8s1a", "v2n32s1", "v2n2s1"])
+def test_fused_seed_every_launch_form(kname, path, fused):
+    """Fused and separate a1 on every launch form (natural order on a ring, time-parallel
+    chunks, epoch order, forced chunks, the e2e double buffer, zero-copy, the host array, a
+    caller device buffer on another stream): the whole stream and the final state, vs the
+    oracle, on a ragged handle with a non-zero gid offset."""
+    n, gb = 9000 if path == "time_parallel" else 70001, 1233  # count 68768: 32-B rows (zero-copy), ragged pieces
+    i = 700 if path == "time_parallel" else 9
+    out, st = _run_path(path, kname, fused, 0, n, i, SEED_PARITY, gid_begin=gb)
+    want = oracle.stream(n, i, SEED_PARITY, gb, n - gb)
+    assert np.array_equal(out, want), (kname, path, fused)
+    assert np.array_equal(st, want[-1])
+
+
+@pytest.mark.parametrize("path", ["ring", "time_parallel", "epoch", "e2e", "host"])
+def test_fused_seed_star_output(path):
+    """The scrambled output (NEXT-3) starting from fused seeds (the state stays unscrambled)."""
+    n, i = (5000, 600) if path == "time_parallel" else (33333, 7)
+    out, st = _run_path(path, "auto", 1, 1, n, i, 77)
+    assert np.array_equal(out, oracle.stream_star(n, i, 77))
+    assert np.array_equal(st, oracle.stream(n, i, 77)[-1])
+
+
+def test_fused_seed_read_state_right_after_init():
+    """prng_read_state between prng_init and the first generate runs the pending seed
+    kernel: it returns the seeds (iteration 0), and generation then continues bit-exactly;
+    a second init re-arms the pending seeds."""
+    n, seed = 4097, 21
+    want = oracle.stream(n, 5, seed)
+    h = P.prng_create(n, seed)
+    try:
+        P.prng_init(h)
+        assert np.array_equal(P.prng_read_state(h, n), want[0])
+        P.prng_generate(h, 5)
+        assert np.array_equal(P.prng_read_state(h, n), want[4])
+        P.prng_init(h)  # pending again: the next launch seeds in registers
+        out = np.zeros((5, n), np.uint64)
+        P.prng_generate(h, 5, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), n, 0, 5, 0))
+        assert np.array_equal(out, want)
+    finally:
+        P.prng_destroy(h)
+
+
+def test_fused_seed_option_roundtrip_and_errors():
+    h = P.prng_create(100, 0)
+    try:
+        assert P.prng_get_option(h, P.PRNG_OPT_FUSED_SEED) == 1
+        P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, 0)
+        assert P.prng_get_option(h, P.PRNG_OPT_FUSED_SEED) == 0
+        for bad in (-1, 2):
+            with pytest.raises(P.PrngError) as e:
+                P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, bad)
+            assert e.value.code == P.PRNG_EINVAL
+    finally:
+        P.prng_destroy(h)
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+def test_fused_seed_top_of_gid_range_and_a3(fused):
+    """Fused seeding hashes the GLOBAL gid (gid_begin + handle-relative index) up to 2^32 - 1,
+    including the A3 zero -> 1 fix-up at the derived trigger gid."""
+    n = 1 << 32
+    gb, cnt = A3_GID - 700, 1500
+    out, st = _run_path("ring", "auto", fused, 0, n, 3, A3_SEED, gid_begin=gb, count=cnt)
+    assert out[0][700] == 1
+    assert np.array_equal(out, oracle.stream(n, 3, A3_SEED, gb, cnt))
+    gb2 = (1 << 32) - 999
+    out2, st2 = _run_path("e2e", "auto", fused, 0, n, 4, 5, gid_begin=gb2, count=999)
+    want2 = oracle.stream(n, 4, 5, gb2, 999)
+    assert np.array_equal(out2, want2) and np.array_equal(st2, want2[-1])
