@@ -91,6 +91,17 @@ def workload(numrn_total: int, numiter: int, e2e_numiter: int, world: int) -> di
             "scaling": "strong", "per_gpu": per}
 
 
+def config_of(W: dict, a, world: int) -> dict:
+    """The `config` object of both arms' lines (identical, so the driver can pair them):
+    the workload and its shape only -- runtime facts (NUMA binding, the oracle's sample)
+    go elsewhere in the line."""
+    return {"workload": W["workload"], "numrn": W["numrn"], "numiter": W["numiter"], "per_gpu": W["per_gpu"],
+            "seed": a.seed, "parallelism": f"gid-shard{world}",
+            "output": ["state (paper)", "xorshift64* scrambled"][a.output],
+            "l2": "output through a 64 GiB rotating ring per GPU (> 500x L2; no address rewritten "
+                  "within 64 GiB, see profiles/r1_ring_absorption.md); no flush needed"}
+
+
 def cpu_model() -> str:
     """The host CPU model (lscpu "Model name", else /proc/cpuinfo), for the baseline lines."""
     import subprocess
@@ -373,8 +384,7 @@ def run_reference(a, D):
         "unit": "numbers/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": W["scaling"],
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (numrn, numiter, seed)",
-        "config": {"workload": W["workload"], "numrn": numrn, "numiter": W["numiter"], "seed": a.seed,
-                   "sampled": True},
+        "config": config_of(W, a, D.world),
         "cpu_baseline": {"value": v, "unit": "numbers/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": v, "unit": "numbers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -593,12 +603,7 @@ def run_ours(a, D):
             "ms_per_step": ms_max / a.steps, "higher_is_better": True,
             "scaling": W["scaling"], "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (numrn, numiter, seed); outputs are the generated u64 stream",
-            "config": {"workload": W["workload"], "numrn": numrn, "numiter": numiter, "per_gpu": cnt, "seed": a.seed,
-                       "parallelism": f"gid-shard{D.world}",
-                       "output": ["state (paper)", "xorshift64* scrambled"][a.output],
-                       "numa_bind": numa,
-                       "l2": "output through a 64 GiB rotating ring per GPU (> 500x L2; no address rewritten "
-                             "within 64 GiB, see profiles/r1_ring_absorption.md); no flush needed"},
+            "config": config_of(W, a, D.world), "host": {"numa_bind": numa},
             "roofline": roofline, "sustained": sustained, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "probes": probes,
         }

@@ -46,6 +46,12 @@ def test_reference_arm_single_process():
     lines = _lines(r.stdout)
     assert len(lines) == 1
     _check(lines[0], 1)
+    # the same `config` object our arm prints for these flags (bench.config_of), so the two
+    # arms' lines pair up: the oracle's bounded sample is described in cpu_baseline.sample
+    sys.path.insert(0, ROOT)
+    import bench
+    want = bench.config_of(bench.workload(65536, 0, 0, 1), type("A", (), {"seed": bench.SEED_PERF, "output": 0}), 1)
+    assert lines[0]["config"] == want, (lines[0]["config"], want)
 
 
 @pytest.mark.parametrize("world", [2, 4])

@@ -54,7 +54,11 @@ def test_bench_line_contract():
     assert e["d2h_bytes_per_step"] == 8 * (1 << 22) * 200 and e["h2d_bytes_per_step"] == 0 and e["value"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(b["clocks"])
     assert b["clocks"]["sm_mhz"] and b["clocks"]["sm_max_mhz"]   # NVML found this CUDA device (by PCI bus id)
-    assert "cpus" in (b["config"]["numa_bind"] or {}), b["config"]["numa_bind"]
+    assert "cpus" in (b["host"]["numa_bind"] or {}), b["host"]["numa_bind"]
+    sys.path.insert(0, ROOT)
+    import bench  # the reference arm prints this same config object (tests/test_bench_cpu.py)
+    assert b["config"] == bench.config_of(bench.workload(1 << 22, 200, 200, 1),
+                                          type("A", (), {"seed": bench.SEED_PERF, "output": 0}), 1)
 
 
 def test_bench_two_ranks_share_one_gpu():
