@@ -16,7 +16,7 @@ import paper_1609_01257_b200 as P  # noqa: E402
 
 names = [P.prng_kernel_variant_name(i) for i in range(P.prng_kernel_variants())]
 cases = [  # (n, iters, variant, mode, output, device-ring slots, PRNG_OPT_EPOCH_ITERS)
-    (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 1000, 0),  # time-parallel chunks (iters >= 512)
+    (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 1000, 0),  # time-parallel chunks
     (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 16, 0),    # wrapping ring: epoch order, E = 16
     (1003, 9, "v4n4s1", P.PRNG_MODE_OVERLAP1, 1, 16, 0),      # star output, ragged n
     (4100, 7, "v4n4s1p", P.PRNG_MODE_SERIAL, 0, 16, 0),       # ping-pong hot loop
@@ -29,9 +29,19 @@ cases = [  # (n, iters, variant, mode, output, device-ring slots, PRNG_OPT_EPOCH
     (4100, 700, "auto", P.PRNG_MODE_OVERLAP2, 1, 1000, 0),    # time-parallel at 8 warps/SM, v2n2s1, star
     (20000, 300, "v4n4s1p", P.PRNG_MODE_ZEROCOPY, 0, 300, 0), # time-parallel from 256 iterations, O3
 ]
+# a1 is fused into the first batch launch by default (seeds computed in registers); these
+# cases also run with the separate seed kernel (PRNG_OPT_FUSED_SEED 0), and every other case
+# reads the state between prng_init and the device-only generate (the pending seeds are
+# then materialised by seed_kernel and the launch does not seed)
+cases = [c + (1,) for c in cases] + [
+    (70001, 40, "auto", P.PRNG_MODE_OVERLAP2, 1, 16, 7, 0),   # separate a1: epochs, star
+    (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 1000, 0, 0),  # separate a1: time-parallel
+    (4100, 7, "v4n4s1p", P.PRNG_MODE_SERIAL, 0, 16, 0, 0),    # separate a1: ping-pong
+]
 bad = 0
-for n, it, v, mode, out, slots, epoch in cases:
+for ci, (n, it, v, mode, out, slots, epoch, fused) in enumerate(cases):
     h = P.prng_create(n, 3)
+    P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, fused)
     P.prng_set_option(h, P.PRNG_OPT_KERNEL, names.index(v))
     P.prng_set_option(h, P.PRNG_OPT_OUTPUT, out)
     P.prng_set_option(h, P.PRNG_OPT_MODE, mode)
@@ -44,10 +54,12 @@ for n, it, v, mode, out, slots, epoch in cases:
     want = oracle.stream_star(n, it, 3) if out else oracle.stream(n, it, 3)
     ok = np.array_equal(buf, want)
     P.prng_init(h)
+    if ci % 2:
+        ok = ok and np.array_equal(P.prng_read_state(h, n), oracle.stream(n, 1, 3)[0])  # materialised seeds
     P.prng_generate(h, it)  # device only through the ring
     ok = ok and np.array_equal(P.prng_read_state(h, n), oracle.stream(n, it, 3)[-1])
     vid, e = P.prng_last_launch(h)
     P.prng_destroy(h)
-    print(n, it, v, mode, out, slots, epoch, "ran", names[vid], "E", e, "ok" if ok else "MISMATCH", flush=True)
+    print(n, it, v, mode, out, slots, epoch, "fused", fused, "ran", names[vid], "E", e, "ok" if ok else "MISMATCH", flush=True)
     bad += not ok
 sys.exit(1 if bad else 0)
