@@ -271,7 +271,9 @@ const char *prng_event_name(uint32_t id);
  * name id, start and end in seconds from a common origin (device intervals from CUDA
  * events; OUT intervals from the host clock aligned to the same origin).  `n_out` gets
  * the number available; at most `cap` are written.  `wall_s` (may be NULL) gets the host
- * wall time of the profiled calls. */
+ * wall time of the profiled calls.  An INIT_KERNEL interval exists only when the seed
+ * kernel ran on its own (PRNG_OPT_FUSED_SEED 0, or a materialising call); with a1 fused
+ * the seeding is inside the first RNG_KERNEL interval. */
 int prng_prof_events(const prng_t *h, uint64_t cap, uint32_t *name_id, double *start_s,
                      double *end_s, uint64_t *n_out, double *wall_s, prng_err_t *err);
 
