@@ -96,6 +96,11 @@ struct prng {
 
     cudaStream_t s_gen = nullptr, s_copy = nullptr;
     bool own_streams = true;
+    // ordering events of the end-to-end pipelines (gen -> copy, copy -> gen), created on
+    // first use and reused by every later call (creating 8-16 events per call cost tens of
+    // microseconds at small n); calls on one handle never overlap, so one pool suffices
+    static constexpr int kPipeEvents = 16;
+    cudaEvent_t pev[kPipeEvents] = {};
 
     // options
     int mode = PRNG_MODE_OVERLAP2;
@@ -148,6 +153,8 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
 int check_handle(prng *h, prng_err_t *err, bool need_init);
 // Run the pending a1 (seed_kernel into d_state on s_gen) if prng_init deferred it.
 int materialize_seeds(prng *h, prng_err_t *err);
+// The handle's pipeline events (prng::pev), created on the first call that needs them.
+int pipeline_events(prng *h, prng_err_t *err);
 // prng_pipeline.cu: the end-to-end modes (S0, S1, O1, O2, O3) of prng_generate with a sink.
 int generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void *user, prng_err_t *err);
 

@@ -370,6 +370,12 @@ static int seed_launch(prng *h, prng_err_t *err) {
     return prof_end(h, h->s_gen, err);
 }
 
+int pipeline_events(prng *h, prng_err_t *err) {
+    for (auto &e : h->pev)
+        if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return PRNG_OK;
+}
+
 int materialize_seeds(prng *h, prng_err_t *err) {
     if (!h->seed_pending) return PRNG_OK;
     if (int rc = seed_launch(h, err)) return rc;
@@ -500,6 +506,8 @@ void prng_destroy(prng_t *h) {
     if (h->s_copy) cudaStreamSynchronize(h->s_copy);
     clear_prof(h);
     free_e2e(h);
+    for (auto &e : h->pev)
+        if (e) cudaEventDestroy(e);
     if (h->d_ring) cudaFree(h->d_ring);
     if (h->d_state) cudaFree(h->d_state);
     if (h->d_state2) cudaFree(h->d_state2);

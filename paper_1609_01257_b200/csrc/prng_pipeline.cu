@@ -81,8 +81,8 @@ static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, uint64_t T_a
     const uint64_t nb = (numiter + T - 1) / T;
     const uint64_t pos0 = h->pos;
     auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    for (auto &e : ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (int rc = pipeline_events(h, err)) return rc;
+    cudaEvent_t *const ev = h->pev;  // ev[0], ev[1]: gen(j) done, per host half
     int rc = PRNG_OK;
     auto gen = [&](uint64_t j) -> int {
         if (int r = launch_batch(h, h->h_dev[j & 1], h->count, T, 0, iters_of(j), pos0 + j * T == 0, h->s_gen, err))
@@ -107,8 +107,6 @@ static int generate_zerocopy(prng *h, uint64_t numiter, uint64_t T, uint64_t T_a
         if (j + 2 < nb) rc = gen(j + 2);
     }
     const cudaError_t es = cudaStreamSynchronize(h->s_gen);
-    for (auto &e : ev)
-        if (e) cudaEventDestroy(e);
     if (!rc && es != cudaSuccess) rc = set_err(err, PRNG_ECUDA, "generation stream: %s", cudaGetErrorString(es));
     if (rc) {
         h->poisoned = true;
@@ -178,26 +176,10 @@ int prng_detail::generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void
 
     // Overlapped modes (S1, O1, O2): gen stream + copy stream + events.
     const int R = 8;  // event ring; at most gen(j+4) / copy(j+2) ahead of the host at batch j
-    cudaEvent_t ev_gen[R], ev_cp[R];
-    for (int i = 0; i < R; ++i) {
-        ev_gen[i] = ev_cp[i] = nullptr;
-    }
+    if (int rc = pipeline_events(h, err)) return rc;
+    cudaEvent_t *const ev_gen = h->pev, *const ev_cp = h->pev + R;
+    static_assert(2 * R <= prng::kPipeEvents, "event pool too small");
     int rc = PRNG_OK;
-    auto cleanup = [&]() {
-        for (int i = 0; i < R; ++i) {
-            if (ev_gen[i]) cudaEventDestroy(ev_gen[i]);
-            if (ev_cp[i]) cudaEventDestroy(ev_cp[i]);
-        }
-    };
-    for (int i = 0; i < R; ++i) {
-        cudaError_t e1 = cudaEventCreateWithFlags(&ev_gen[i], cudaEventDisableTiming);
-        cudaError_t e2 = cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming);
-        if (e1 != cudaSuccess || e2 != cudaSuccess) {
-            cleanup();
-            h->poisoned = true;
-            return set_err(err, PRNG_ECUDA, "cudaEventCreate failed");
-        }
-    }
     uint64_t gen_enq = 0, cp_enq = 0;  // batches enqueued so far
     auto enqueue_gen = [&](uint64_t j) -> int {
         // gen(j) overwrites device half j%2, last read by copy(j-2)  (WAR, A15)
@@ -246,12 +228,10 @@ int prng_detail::generate_e2e(prng *h, uint64_t numiter, prng_sink_fn sink, void
     if (rc) {
         cudaStreamSynchronize(h->s_gen);
         cudaStreamSynchronize(h->s_copy);
-        cleanup();
         h->poisoned = true;
         return rc;
     }
     const cudaError_t es = cudaStreamSynchronize(h->s_gen);
-    cleanup();
     if (es != cudaSuccess) {
         h->poisoned = true;
         return set_err(err, PRNG_ECUDA, "generation stream: %s", cudaGetErrorString(es));
@@ -292,7 +272,11 @@ int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_
     const uint64_t nb = (numiter + T - 1) / T, pitch = h->buf_pitch, pos0 = h->pos;
     auto iters_of = [&](uint64_t j) { return (uint32_t)std::min<uint64_t>(T, numiter - j * T); };
     const int R = 4;
-    cudaEvent_t ev_gen[R] = {}, ev_cp[R] = {};
+    if (int r = pipeline_events(h, err)) {
+        if (registered_here) cudaHostUnregister(dst);
+        return r;
+    }
+    cudaEvent_t *const ev_gen = h->pev, *const ev_cp = h->pev + R;
     int rc = PRNG_OK;
     // every CUDA call of the pipeline is checked: a failed record / wait would otherwise let
     // a copy run before its generation (or a generation overwrite a half still being read)
@@ -302,10 +286,6 @@ int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_
         return set_err(err, e == cudaErrorMemoryAllocation ? PRNG_ENOMEM : PRNG_ECUDA, "%s: %s", what,
                        cudaGetErrorString(e));
     };
-    for (int i = 0; i < R && !rc; ++i) {
-        rc = chk(cudaEventCreateWithFlags(&ev_gen[i], cudaEventDisableTiming), "cudaEventCreate");
-        if (!rc) rc = chk(cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming), "cudaEventCreate");
-    }
     const double t0 = now_s();
     for (uint64_t j = 0; j < nb && !rc; ++j) {
         // gen(j) into device half j%2, after copy(j-2) has drained it (WAR, A15)
@@ -336,10 +316,6 @@ int prng_generate_host(prng_t *h, uint64_t numiter, uint64_t *dst, uint64_t dst_
     }
     const cudaError_t eg = cudaStreamSynchronize(h->s_gen);
     const cudaError_t ec = cudaStreamSynchronize(h->s_copy);
-    for (int i = 0; i < R; ++i) {
-        if (ev_gen[i]) cudaEventDestroy(ev_gen[i]);
-        if (ev_cp[i]) cudaEventDestroy(ev_cp[i]);
-    }
     if (registered_here) cudaHostUnregister(dst);
     if (!rc) rc = chk(eg, "generation stream");
     if (!rc) rc = chk(ec, "copy stream");
