@@ -862,7 +862,8 @@ def test_argument_errors_on_a_live_handle():
 def test_randomised_configurations():
     """Seeded fuzz over the option space: numrn, numiter, seed, mode, batch size, kernel
     variant, output transform, time-parallel on/off, epoch order (auto / off / forced E),
-    piece order, jump-started chunks, and how the run is split into calls; end to end
+    piece order, jump-started chunks, fused or separate a1, and how the run is split into
+    calls; end to end
     (every output) or device only (the ring slots still held, small rings that wrap);
     every value vs the oracle."""
     r = np.random.default_rng(20261017)
@@ -887,15 +888,16 @@ def test_randomised_configurations():
         slots = int(r.choice([1, 2, 5, 16, 1000]))
         cuts = sorted({int(c) for c in r.integers(1, i, size=2)}) if i > 2 else []
         calls = [b - a for a, b in zip([0] + cuts, cuts + [i])]
+        fused = int(r.random() < 0.7)
         cfg = dict(trial=trial, n=n, i=i, mode=mode, kernel=names[kv], star=star, tp=tp, batch=batch, epoch=epoch,
-                   order=order, chunk=chunk, device_only=device_only, slots=slots, calls=calls)
+                   order=order, chunk=chunk, device_only=device_only, slots=slots, calls=calls, fused=fused)
         want = oracle.stream_star(n, i, seed) if star else oracle.stream(n, i, seed)
         h = P.prng_create(n, seed)
         try:
             for opt, val in [(P.PRNG_OPT_MODE, mode), (P.PRNG_OPT_KERNEL, kv), (P.PRNG_OPT_OUTPUT, star),
                              (P.PRNG_OPT_TIME_PARALLEL, tp), (P.PRNG_OPT_BATCH_ITERS, batch),
                              (P.PRNG_OPT_EPOCH_ITERS, epoch), (P.PRNG_OPT_PIECE_ORDER, order),
-                             (P.PRNG_OPT_CHUNK_ITERS, chunk)]:
+                             (P.PRNG_OPT_CHUNK_ITERS, chunk), (P.PRNG_OPT_FUSED_SEED, fused)]:
                 P.prng_set_option(h, opt, val)
             if device_only:
                 P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, slots)
@@ -1290,7 +1292,8 @@ def test_randomised_api_sequences():
     """Seeded fuzz over sequences of C-ABI calls on one handle: prng_init / prng_seek, then a
     random mix of prng_generate (sink or device-only ring), prng_generate_device (into a
     torch buffer, random pitch and slot count) and prng_generate_host (random row ring),
-    with random variant / output / time-parallel options; after every call the emitted
+    with random variant / output / time-parallel / fused-seed options (and, sometimes, a
+    state read between prng_init and the first generate); after every call the emitted
     iterations (and the state) are compared with the oracle's stream at those positions."""
     import torch
     r = np.random.default_rng(777)
@@ -1309,10 +1312,13 @@ def test_randomised_api_sequences():
             P.prng_set_option(h, P.PRNG_OPT_OUTPUT, star)
             P.prng_set_option(h, P.PRNG_OPT_TIME_PARALLEL, int(r.random() < 0.8))
             P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, int(r.choice([0, 1, 3, 64])))
+            P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, int(r.random() < 0.7))
             if start:
                 P.prng_seek(h, start)
             else:
                 P.prng_init(h)
+                if r.random() < 0.3:  # the pending seeds, materialised by the read
+                    assert np.array_equal(P.prng_read_state(h), plain[0]), trial
             pos = start
             while pos < total:
                 m = int(min(total - pos, r.choice([1, 2, 9, 130, 300])))
