@@ -61,18 +61,26 @@ def test_bench_line_contract():
                                           type("A", (), {"seed": bench.SEED_PERF, "output": 0}), 1)
 
 
-def test_bench_two_ranks_share_one_gpu():
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
-                        "--dist-backend", "gloo", "--device-mod", "1", "--no-e2e", *SMALL],
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_ranks_share_one_gpu(world):
+    """The driver's N > 1 launch (torchrun, one process per rank) with every rank on the one
+    GPU over gloo: barrier + MAX-over-ranks timing, per-rank e2e, rank 0 alone prints
+    (timings meaningless: the ranks share a GPU; the probes are in the slow N = 2 test)."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus",
+                        str(world), "--dist-backend", "gloo", "--device-mod", "1", *SMALL, "--e2e-steps", "1",
+                        "--e2e-warmup", "0"],
                        cwd=ROOT, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stderr
+    assert r.returncode == 0, r.stderr[-3000:]
     lines = _lines(r.stdout)
     assert len(lines) == 1  # rank 0 alone prints
     b = lines[0]
-    assert b["n_gpus"] == 2 and b["metric"] == _metric() and b["scaling"] == "strong" and b["value"] > 0
-    assert b["config"]["numrn"] == 1 << 22 and b["config"]["per_gpu"] == 1 << 21
-    assert b["config"]["parallelism"] == "gid-shard2"
+    assert b["n_gpus"] == world and b["metric"] == _metric() and b["scaling"] == "strong" and b["value"] > 0
+    assert b["config"]["numrn"] == 1 << 22 and b["config"]["per_gpu"] == (1 << 22) // world
+    assert b["config"]["parallelism"] == f"gid-shard{world}"
+    assert b["gpu_launches"] == b["steps"]  # rank 0's own launches (one fused launch per step)
+    e = b["e2e"]
+    assert e["d2h_bytes_per_step"] == 8 * (1 << 22) * 200 and e["value"] > 0
 
 
 @pytest.mark.slow
