@@ -572,7 +572,7 @@ def test_chunks_never_race_on_a_wrapping_ring(slots, chunk):
     """Time-parallel chunks of one piece run on different warps at once; on a ring with
     fewer slots than the launch's iterations two chunks would write the same slot, so the
     library keeps chunking to launches that do not wrap.  Small numrn (time-parallel by
-    default at >= 512 iterations) and forced chunks through wrapping rings: the last R
+    default from 144 iterations: >= 3 chunks of >= 48) and forced chunks through wrapping rings: the last R
     iterations and the state vs the oracle."""
     n, i = 100, 1000
     want = oracle.stream(n, i, 21)

@@ -27,7 +27,7 @@ cases = [  # (n, iters, variant, mode, output, device-ring slots, PRNG_OPT_EPOCH
     (300000, 9, "v4n16s1", P.PRNG_MODE_OVERLAP2, 1, 16, 0),   # wide pieces, ragged last piece
     (3000, 9, "auto", P.PRNG_MODE_OVERLAP2, 0, 16, 0),        # auto -> v2n2s1 (small handle), ragged
     (4100, 700, "auto", P.PRNG_MODE_OVERLAP2, 1, 1000, 0),    # time-parallel at 8 warps/SM, v2n2s1, star
-    (20000, 300, "v4n4s1p", P.PRNG_MODE_ZEROCOPY, 0, 300, 0), # time-parallel from 256 iterations, O3
+    (20000, 300, "v4n4s1p", P.PRNG_MODE_ZEROCOPY, 0, 300, 0), # time-parallel (>= 3 chunks of >= 48), O3
 ]
 # a1 is fused into the first batch launch by default (seeds computed in registers); these
 # cases also run with the separate seed kernel (PRNG_OPT_FUSED_SEED 0), and every other case
