@@ -317,23 +317,9 @@ int prng_prof_export(uint64_t nevents, const uint32_t *name_id, const double *st
                      const double *end_s, uint32_t nnames, const char *const *names,
                      const char *const *queues, const char *path, prng_err_t *err);
 
-/* ------------------------------------------------------------------ roofline probes */
-/* Same-box denominators, for bench.py: each returns GB/s or < 0 on
- * error; `bytes` is the buffer size.  The store kernels write pseudo-random
- * (incompressible) data, like the generator. */
-double prng_probe_memset_gbs(uint64_t bytes, int reps);  /* cudaMemsetAsync (copy engine), best of reps */
-/* The same fill repeated `reps` times back to back, timed as one interval (sustained,
- * power-capped write rate of the fill engine). */
-double prng_probe_memset_sustained_gbs(uint64_t bytes, int reps);
-double prng_probe_store_gbs(uint64_t bytes, int reps);   /* persistent grid-stride 32-B store sweep */
-/* One-shot grid of 128-thread CTAs, each writing one contiguous 16 KiB chunk with 32-B
- * stores (a framework fill kernel's structure): the fastest SM write pattern measured. */
-double prng_probe_fill_gbs(uint64_t bytes, int reps);
-/* Pinned (or pageable) cudaMemcpyAsync D2H over `nstreams` streams, best of `reps`. */
-double prng_probe_d2h_gbs(uint64_t bytes, int reps, int pinned, int nstreams);
-/* `reps` pinned D2H copies back to back timed as one interval: each rank's sustained share
- * of the host links when all ranks of a node run it at once (bench.py, N > 1). */
-double prng_probe_d2h_sustained_gbs(uint64_t bytes, int reps);
+/* The same-box roofline probes bench.py divides by (memset, SM fill / store kernels, D2H
+ * host link) are measurement tools, not part of the hot path: they live in their own
+ * library, libprng_probes.so (include/prng_probes.h). */
 
 #ifdef __cplusplus
 }

@@ -12,10 +12,10 @@ import os
 
 import numpy as np
 
-from ._build import LIB, build as _build_lib
+from ._build import LIB, PROBES_LIB, build as _build_lib
 
 __all__ = [
-    "PrngError", "lib", "prng_create", "prng_create_range", "prng_destroy", "prng_get_range", "prng_init",
+    "PrngError", "lib", "probes_lib", "prng_create", "prng_create_range", "prng_destroy", "prng_get_range", "prng_init",
     "prng_generate", "prng_generate_device", "prng_generate_host", "prng_seek", "prng_device_ring", "prng_read_slot",
     "prng_read_state", "prng_set_option", "prng_get_option", "prng_set_streams",
     "prng_strerror", "prng_prof_events", "prng_prof_calc", "prng_event_name",
@@ -106,12 +106,6 @@ def lib():
         "prng_prof_calc": ([u64, vp, vp, vp, u32, dbl, vp, vp, PD, PD, E], i32),
         "prng_prof_summary": ([u64, vp, vp, vp, u32, vp, dbl, i32, i32, vp, u64, P64, E], i32),
         "prng_prof_export": ([u64, vp, vp, vp, u32, vp, vp, ctypes.c_char_p, E], i32),
-        "prng_probe_memset_gbs": ([u64, i32], dbl),
-        "prng_probe_memset_sustained_gbs": ([u64, i32], dbl),
-        "prng_probe_store_gbs": ([u64, i32], dbl),
-        "prng_probe_fill_gbs": ([u64, i32], dbl),
-        "prng_probe_d2h_gbs": ([u64, i32, i32, i32], dbl),
-        "prng_probe_d2h_sustained_gbs": ([u64, i32], dbl),
         "prng_sink_null": ([vp, u64, u32, u64, u64, P64], i32),
         "prng_sink_copy": ([vp, u64, u32, u64, u64, P64], i32),
         "prng_sink_digest": ([vp, u64, u32, u64, u64, P64], i32),
@@ -120,6 +114,34 @@ def lib():
         f = getattr(L, name)
         f.argtypes, f.restype = args, res
     _lib = L
+    return L
+
+
+_probes = None
+
+
+def probes_lib():
+    """Load libprng_probes.so: bench.py's same-box roofline probes (include/prng_probes.h),
+    a library of its own, apart from the hot path's libprng_b200.so."""
+    global _probes
+    if _probes is not None:
+        return _probes
+    lib()  # builds both libraries when their sources are newer
+    if not os.path.exists(PROBES_LIB):
+        raise PrngError(PRNG_ECUDA, f"{PROBES_LIB} missing: the probes are not built")
+    L = ctypes.CDLL(PROBES_LIB)
+    sig = {
+        "prng_probe_memset_gbs": ([u64, i32], dbl),
+        "prng_probe_memset_sustained_gbs": ([u64, i32], dbl),
+        "prng_probe_store_gbs": ([u64, i32], dbl),
+        "prng_probe_fill_gbs": ([u64, i32], dbl),
+        "prng_probe_d2h_gbs": ([u64, i32, i32, i32], dbl),
+        "prng_probe_d2h_sustained_gbs": ([u64, i32], dbl),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes, f.restype = args, res
+    _probes = L
     return L
 
 
@@ -390,24 +412,24 @@ def prng_prof_export(path: str, name_id, start_s, end_s, nnames: int = 4, names=
 
 
 def prng_probe_memset_gbs(nbytes: int, reps: int = 5) -> float:
-    return lib().prng_probe_memset_gbs(nbytes, reps)
+    return probes_lib().prng_probe_memset_gbs(nbytes, reps)
 
 
 def prng_probe_memset_sustained_gbs(nbytes: int, reps: int = 100) -> float:
-    return lib().prng_probe_memset_sustained_gbs(nbytes, reps)
+    return probes_lib().prng_probe_memset_sustained_gbs(nbytes, reps)
 
 
 def prng_probe_store_gbs(nbytes: int, reps: int = 5) -> float:
-    return lib().prng_probe_store_gbs(nbytes, reps)
+    return probes_lib().prng_probe_store_gbs(nbytes, reps)
 
 
 def prng_probe_fill_gbs(nbytes: int, reps: int = 5) -> float:
-    return lib().prng_probe_fill_gbs(nbytes, reps)
+    return probes_lib().prng_probe_fill_gbs(nbytes, reps)
 
 
 def prng_probe_d2h_gbs(nbytes: int, reps: int = 5, pinned: bool = True, nstreams: int = 1) -> float:
-    return lib().prng_probe_d2h_gbs(nbytes, reps, int(pinned), nstreams)
+    return probes_lib().prng_probe_d2h_gbs(nbytes, reps, int(pinned), nstreams)
 
 
 def prng_probe_d2h_sustained_gbs(nbytes: int, reps: int = 8) -> float:
-    return lib().prng_probe_d2h_sustained_gbs(nbytes, reps)
+    return probes_lib().prng_probe_d2h_sustained_gbs(nbytes, reps)

@@ -1,4 +1,5 @@
-"""Build libprng_b200.so in-tree with nvcc for sm_100a (no JIT, no torch extension cache)."""
+"""Build libprng_b200.so (the hot path's C ABI) and libprng_probes.so (bench.py's same-box
+roofline probes) in-tree with nvcc for sm_100a (no JIT, no torch extension cache)."""
 from __future__ import annotations
 
 import os
@@ -10,9 +11,12 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libprng_b200.so")
 SOURCES = [os.path.join(CSRC, f) for f in
-           ("prng_engine.cu", "prng_pipeline.cu", "prng_probes.cu", "prng_prof.cpp", "prng_sinks.cpp")]
+           ("prng_engine.cu", "prng_pipeline.cu", "prng_prof.cpp", "prng_sinks.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "prng_kernels.cuh"), os.path.join(CSRC, "engine_internal.h"),
                   os.path.join(ROOT, "include", "prng.h"), os.path.join(ROOT, "include", "prng_sinks.h")]
+PROBES_LIB = os.path.join(PKG, "libprng_probes.so")
+PROBES_SOURCES = [os.path.join(CSRC, "prng_probes.cu")]
+PROBES_DEPS = PROBES_SOURCES + [os.path.join(ROOT, "include", "prng_probes.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
@@ -52,7 +56,23 @@ def build_cli(force: bool = False) -> str:
     return CLI
 
 
+def build_probes(force: bool = False) -> str:
+    """libprng_probes.so: measurement probes only, no code shared with libprng_b200.so."""
+    if not force and os.path.exists(PROBES_LIB) and all(
+            os.path.getmtime(d) <= os.path.getmtime(PROBES_LIB) for d in PROBES_DEPS):
+        return PROBES_LIB
+    tmp = PROBES_LIB + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *PROBES_SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed ({r.returncode}): {' '.join(cmd)}")
+    os.replace(tmp, PROBES_LIB)
+    return PROBES_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_probes(force)
     if not force and not needs_build():
         build_cli()
         return LIB

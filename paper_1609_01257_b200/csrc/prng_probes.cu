@@ -1,4 +1,5 @@
-// prng_probes.cu -- same-box roofline denominators: the copy-engine
+// prng_probes.cu -- libprng_probes.so (include/prng_probes.h), same-box roofline
+// denominators, built apart from libprng_b200.so: the copy-engine
 // memset fill, two SM store kernels over pseudo-random (incompressible) data, and the
 // pinned / pageable D2H host link (alone, or sustained while other ranks copy too).
 #include <cuda_runtime.h>
@@ -9,11 +10,17 @@
 #include <cstring>
 #include <vector>
 
-#include "engine_internal.h"
+#include <chrono>
 
-using namespace prng_detail;
+#include "../../include/prng_probes.h"
 
 namespace probek {
+
+constexpr int kBlock = 256;  // threads per CTA of the store sweep
+
+inline double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 // Self-contained helpers: the probes measure the hardware, not the method.
 __device__ __forceinline__ void st4(uint64_t *p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
@@ -114,9 +121,9 @@ double prng_probe_store_gbs(uint64_t bytes, int reps) {
     int dev = 0, sms = 0, bps = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, probek::store_probe_kernel, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, probek::store_probe_kernel, probek::kBlock, 0);
     const double best = probek::best_gbs(bytes, reps, [&](int) {
-        probek::store_probe_kernel<<<sms * std::max(bps, 1), kBlock>>>(p, bytes / 32);
+        probek::store_probe_kernel<<<sms * std::max(bps, 1), probek::kBlock>>>(p, bytes / 32);
     });
     cudaFree(p);
     return cudaGetLastError() == cudaSuccess ? best : -1;
@@ -171,17 +178,17 @@ static double d2h_probe(uint64_t bytes, int reps, int pinned, int nstreams, int 
     if (sustained) {
         copy_once();  // warm-up
         for (auto &s : ss) cudaStreamSynchronize(s);
-        const double t0 = now_s();
+        const double t0 = probek::now_s();
         for (int r = 0; r < reps; ++r) copy_once();
         for (auto &s : ss) cudaStreamSynchronize(s);
-        best = (double)bytes * reps / (now_s() - t0) / 1e9;
+        best = (double)bytes * reps / (probek::now_s() - t0) / 1e9;
     } else {
         for (int r = 0; r < reps + 1; ++r) {
             cudaDeviceSynchronize();
-            const double t0 = now_s();
+            const double t0 = probek::now_s();
             copy_once();
             for (auto &s : ss) cudaStreamSynchronize(s);
-            const double dt = now_s() - t0;
+            const double dt = probek::now_s() - t0;
             if (r) best = std::max(best, bytes / dt / 1e9);
         }
     }

@@ -15,9 +15,9 @@ from oracle import prof as oprof
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared_functions():
+def _declared_functions(headers=("prng.h", "prng_sinks.h")):
     names = set()
-    for h in ("prng.h", "prng_sinks.h"):
+    for h in headers:
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(prng_\w+)\s*\(", src, flags=re.M):
@@ -30,14 +30,34 @@ def test_library_exports_every_declared_symbol():
     declared = _declared_functions()
     assert {"prng_create", "prng_init", "prng_generate", "prng_destroy", "prng_strerror",
             "prng_create_range", "prng_prof_calc", "prng_sink_null"} <= declared
-    out = subprocess.run(["nm", "-D", "--defined-only", P.LIB], capture_output=True, text=True, check=True).stdout
-    exported = {l.split()[-1] for l in out.splitlines() if l.strip()}
+    exported = _exported(P.LIB)
     missing = declared - exported
     assert not missing, f"declared in include/ but not exported: {missing}"
 
 
-def test_library_is_sm100a():
-    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", P.LIB], capture_output=True, text=True).stdout
+def _exported(path):
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True, check=True).stdout
+    return {l.split()[-1] for l in out.splitlines() if l.strip()}
+
+
+def test_probes_are_a_library_of_their_own():
+    """bench.py's roofline probes (include/prng_probes.h) live in libprng_probes.so; the hot
+    path's libprng_b200.so exports none of them, and the probes library none of the hot
+    path's symbols."""
+    P.probes_lib()
+    probes = _declared_functions(("prng_probes.h",))
+    assert {"prng_probe_memset_gbs", "prng_probe_fill_gbs", "prng_probe_d2h_sustained_gbs"} <= probes
+    exported = _exported(P.PROBES_LIB)
+    assert not probes - exported, probes - exported
+    assert not {x for x in _exported(P.LIB) if x.startswith("prng_probe")}
+    assert not {x for x in exported if x.startswith("prng_") and not x.startswith("prng_probe_")}
+
+
+@pytest.mark.parametrize("which", ["LIB", "PROBES_LIB"])
+def test_library_is_sm100a(which):
+    P.probes_lib()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", getattr(P, which)], capture_output=True,
+                         text=True).stdout
     assert "sm_100a" in out
 
 
