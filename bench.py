@@ -482,9 +482,13 @@ def run_ours(a, D):
     if traffic_algo is not None and int(traffic_algo) != algo_bytes:
         traffic = None  # the committed capture is of another shape
     kname = ("prngk::batch_kernel_epoch<" + vname + f", E={epoch}>" if epoch else "prngk::batch_kernel<" + vname + ">")
+    gb_, gt_, gr_, g1_ = P.prng_last_grid(h)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kname,
                 "grid_warps": grid_warps or "variant default", "autotune_probe_gbs": tune_gbs,
+                "grid": {"ctas": gb_, "threads_per_cta": gt_, "rounds_per_warp": gr_,
+                         "form": "one-shot (one piece per warp, CTAs dispatched in order)" if g1_
+                         else "persistent (one wave)"},
                 "algorithmic_bytes_per_launch": algo_bytes, "mean_launch_ms": kmean,
                 "best_launch_ms": min(kern_ms), "median_launch_ms": statistics.median(kern_ms),
                 "achieved_best_launch": algo_bytes / (min(kern_ms) * 1e-3) / 1e9,

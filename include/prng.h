@@ -209,7 +209,7 @@ enum prng_option {
                                   bytes per warp-iteration) are < 2x L2, so no address is
                                   rewritten while its line may still be in L2 (DESIGN.md
                                   §5); E > 0 forced; -1 off.                                */
-    PRNG_OPT_FUSED_SEED = 17   /* 1 (default): prng_init only records that the stream restarts;
+    PRNG_OPT_FUSED_SEED = 17,  /* 1 (default): prng_init only records that the stream restarts;
                                   the next batch launch computes the seeds (a1) in registers
                                   before its first iteration -- one launch and 16 B per
                                   work-item of state traffic less, output unchanged.  Calls
@@ -218,6 +218,19 @@ enum prng_option {
                                   launches the seed kernel itself (the paper's separate
                                   `init` kernel; its interval is INIT_KERNEL in the
                                   profile, as in Fig. 5).                                   */
+    PRNG_OPT_ONE_SHOT = 18     /* grid of natural-order launches with many more pieces than
+                                  one wave of resident warps: 1 (default) auto -- from 5
+                                  waves of the one-shot grid's resident warps on (2^23
+                                  work-items for v4n8s1a), one piece per warp on a
+                                  multi-wave grid of 4-warp CTAs that the hardware
+                                  dispatches in order (measured 2-8 % more write bandwidth
+                                  than the persistent grid from 2^23 work-items, 5 % more
+                                  under the power cap); 0: always the
+                                  persistent one-wave grid; 2: one-shot whenever the launch
+                                  form allows it (natural order, no PRNG_OPT_GRID_WARPS /
+                                  CTA_WARPS / EPOCH_ITERS / CHUNK_ITERS, no L2-absorbing
+                                  ring wrap), for tests and measurements.  Output
+                                  unchanged.  prng_last_grid reports the grid used.        */
 };
 
 /* End-to-end pipelines: two serialised reproductions of the paper's finding, and the two
@@ -257,6 +270,12 @@ const char *prng_kernel_variant_name(int id);
  * default), *epoch_iters = its epoch length (0 = natural order).  -1 / 0
  * before any launch.  Either pointer may be NULL.  PRNG_EINVAL for a NULL handle. */
 int prng_last_launch(const prng_t *h, int *variant, uint32_t *epoch_iters, prng_err_t *err);
+
+/* The grid of the last batch launch: CTAs, threads per CTA, the rounds of units each warp
+ * walks, and whether it was a one-shot grid (PRNG_OPT_ONE_SHOT; rounds is then 1).  Zeros
+ * before any launch.  Any pointer may be NULL.  PRNG_EINVAL for a NULL handle. */
+int prng_last_grid(const prng_t *h, uint64_t *blocks, uint32_t *threads, uint32_t *rounds, int *one_shot,
+                   prng_err_t *err);
 
 /* ------------------------------------------------------------------ profiling (a6) */
 /* Event name ids, as cf4ocl names them in Fig. 3 plus the host sink. */

@@ -25,7 +25,7 @@ __all__ = [
     "CopySink", "DigestSink", "SINK_FN",
     "PRNG_OPT_MODE", "PRNG_OPT_BATCH_ITERS", "PRNG_OPT_RING_SLOTS", "PRNG_OPT_PROFILE",
     "PRNG_OPT_KERNEL", "PRNG_OPT_GRID_WARPS", "PRNG_OPT_RING_PAD", "PRNG_OPT_HOST_MEM", "PRNG_OPT_CHUNK_ITERS",
-    "PRNG_OPT_PIECE_ORDER", "PRNG_OPT_EPOCH_ITERS", "PRNG_OPT_FUSED_SEED", "PRNG_MODE_ZEROCOPY", "PRNG_MODE_SERIAL", "PRNG_MODE_PAGEABLE",
+    "PRNG_OPT_PIECE_ORDER", "PRNG_OPT_EPOCH_ITERS", "PRNG_OPT_FUSED_SEED", "PRNG_OPT_ONE_SHOT", "prng_last_grid", "PRNG_MODE_ZEROCOPY", "PRNG_MODE_SERIAL", "PRNG_MODE_PAGEABLE",
     "PRNG_MODE_OVERLAP1", "PRNG_MODE_OVERLAP2", "EV_NAMES",
 ]
 
@@ -35,6 +35,7 @@ PRNG_OPT_MODE, PRNG_OPT_BATCH_ITERS, PRNG_OPT_RING_SLOTS = 1, 2, 3
 PRNG_OPT_PROFILE, PRNG_OPT_KERNEL, PRNG_OPT_GRID_WARPS, PRNG_OPT_RING_PAD, PRNG_OPT_HOST_MEM = 4, 5, 6, 7, 8
 PRNG_OPT_OUTPUT, PRNG_OPT_TIME_PARALLEL, PRNG_OPT_BLOCKING, PRNG_OPT_CTA_WARPS = 10, 11, 12, 13
 PRNG_OPT_CHUNK_ITERS, PRNG_OPT_PIECE_ORDER, PRNG_OPT_EPOCH_ITERS, PRNG_OPT_FUSED_SEED = 14, 15, 16, 17
+PRNG_OPT_ONE_SHOT = 18
 PRNG_MODE_SERIAL, PRNG_MODE_PAGEABLE, PRNG_MODE_OVERLAP1, PRNG_MODE_OVERLAP2, PRNG_MODE_ZEROCOPY = 0, 1, 2, 3, 4
 EV_NAMES = ("INIT_KERNEL", "RNG_KERNEL", "READ_BUFFER", "OUT")
 
@@ -101,6 +102,7 @@ def lib():
         "prng_kernel_variants": ([], i32),
         "prng_kernel_variant_name": ([i32], ctypes.c_char_p),
         "prng_last_launch": ([vp, ctypes.POINTER(i32), P32, E], i32),
+        "prng_last_grid": ([vp, P64, P32, P32, ctypes.POINTER(i32), E], i32),
         "prng_event_name": ([u32], ctypes.c_char_p),
         "prng_prof_events": ([vp, u64, vp, vp, vp, P64, PD, E], i32),
         "prng_prof_calc": ([u64, vp, vp, vp, u32, dbl, vp, vp, PD, PD, E], i32),
@@ -332,6 +334,16 @@ def prng_last_launch(h):
     v, e = ctypes.c_int(-1), ctypes.c_uint32(0)
     _check(lib().prng_last_launch(h, ctypes.byref(v), ctypes.byref(e), ctypes.byref(err)), err)
     return v.value, e.value
+
+
+def prng_last_grid(h):
+    """(CTAs, threads per CTA, rounds of units per warp, one-shot?) of the handle's last
+    batch launch (PRNG_OPT_ONE_SHOT)."""
+    err = prng_err_t()
+    b, t, r, o = u64(), ctypes.c_uint32(0), ctypes.c_uint32(0), ctypes.c_int(0)
+    _check(lib().prng_last_grid(h, ctypes.byref(b), ctypes.byref(t), ctypes.byref(r), ctypes.byref(o),
+                                ctypes.byref(err)), err)
+    return b.value, t.value, r.value, bool(o.value)
 
 
 def prng_event_name(i: int) -> str:

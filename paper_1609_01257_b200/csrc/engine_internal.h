@@ -44,6 +44,7 @@ inline int ok(prng_err_t *err) {
     } while (0)
 
 constexpr int kBlock = 256;     // threads per CTA of the batch kernels (max)
+constexpr int kOneShotBlock = 128;  // threads per CTA of a one-shot grid (4 warps, measured best)
 constexpr int kMaxVariants = 16;
 
 inline double now_s() {
@@ -117,6 +118,13 @@ struct prng {
     // failed record / wait / copy poisons the handle instead of returning silent output.
     int64_t fault_after = 0;
     int blocks_per_sm[prng_detail::kMaxVariants] = {0};
+    // resident CTAs per SM of each variant at prng_detail::kOneShotBlock threads (one-shot
+    // grids, PRNG_OPT_ONE_SHOT); 0 = not queried yet
+    int oneshot_blocks_per_sm[2][prng_detail::kMaxVariants] = {};  // [output transform][variant]
+    int one_shot = 1;               // PRNG_OPT_ONE_SHOT: 0 off, 1 auto, 2 always (when allowed)
+    uint64_t last_blocks = 0;       // grid of the last batch launch (prng_last_grid)
+    uint32_t last_threads = 0, last_rounds = 0;
+    bool last_one_shot = false;
 
     // profiling (a6)
     cudaEvent_t ev_origin = nullptr;

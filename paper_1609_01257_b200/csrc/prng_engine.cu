@@ -198,6 +198,50 @@ constexpr uint64_t kAutoNarrowBelow = 1ull << 15;
 // work-items (profiles/r2_fig4.md "Round-2 session 3", raw_r2/m25).
 constexpr uint64_t kTpMinChunk = 48;
 
+// One-shot grids (PRNG_OPT_ONE_SHOT, profiles/r2_write_ceiling.md §7): a
+// natural-order launch with many more pieces than one wave of the persistent grid holds
+// runs one piece per warp on a multi-wave grid of 4-warp CTAs, which the hardware
+// dispatches in order as earlier CTAs retire.  Measured on B200 (raw_r2/m32-m35): at 2^23
+// to 2^27 work-items 2-8 % more DRAM write bandwidth than the persistent 4-warps-per-SM
+// grid in a burst, and 5 % more sustained under the power cap (6.79 vs 6.44 TB/s at the
+// bench shape); at 2^21-2^22 (<= 3 waves of v4n8s1a's 5328 resident one-shot warps) 1-5 %
+// slower.  Used from this many waves of resident one-shot warps on (2^23 = 6.2 waves).
+constexpr uint64_t kOneShotMinWaves = 5;
+
+// Resident warps of a one-shot grid of variant vid (occupancy at kOneShotBlock threads of
+// the instantiation this launch will run), queried once per handle.
+static int oneshot_capacity(prng *h, int vid, BatchFn fn, uint64_t *warps, prng_err_t *err) {
+    int &b = h->oneshot_blocks_per_sm[h->output == 1 ? 1 : 0][vid];
+    if (b == 0) {
+        int q = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, fn, kOneShotBlock, 0));
+        b = std::max(q, 1);
+    }
+    *warps = (uint64_t)b * h->num_sms * (kOneShotBlock / 32);
+    return PRNG_OK;
+}
+
+// Whether this launch of variant vid runs on a one-shot grid: the option allows it, the
+// caller fixed neither the grid nor the work order, there are enough pieces (auto: at least
+// kOneShotMinWaves waves), and the resident set does not let a wrapping launch rewrite
+// L2-resident lines (the same live-set test as the persistent grid's, with the one-shot
+// grid's resident warps).
+static int oneshot_launch(prng *h, int vid, uint64_t nslots, uint32_t iters, bool *yes, prng_err_t *err) {
+    *yes = false;
+    if (h->one_shot == 0 || h->grid_warps > 0 || h->cta_warps > 0 || h->epoch_iters > 0 || h->chunk_iters > 0)
+        return PRNG_OK;
+    const Variant &v = kVariants[vid];
+    const uint64_t piece = 32ull * v.npt;
+    const uint64_t npieces = (h->count + piece - 1) / piece;
+    uint64_t cap = 0;
+    if (int rc = oneshot_capacity(h, vid, h->output == 1 ? v.star : v.fn, &cap, err)) return rc;
+    if (h->one_shot == 1 && npieces < kOneShotMinWaves * cap) return PRNG_OK;
+    if (iters > nslots && nslots * std::min(cap, npieces) * piece * sizeof(uint64_t) < 2 * (uint64_t)h->l2_bytes)
+        return PRNG_OK;
+    *yes = true;
+    return PRNG_OK;
+}
+
 static int variant_id(const char *name) {
     for (int i = 0; i < kNumVariants; ++i)
         if (!std::strcmp(kVariants[i].name, name)) return i;
@@ -209,11 +253,15 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
                  bool first_is_state, cudaStream_t s, prng_err_t *err) {
     int vid = h->kernel;
     int wps = 0;  // warps per SM override (anti-absorption, second choice)
+    bool oneshot = false;
     if (vid == 0) {  // "auto"
         vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1a" : h->count >= kAutoNarrowBelow ? "v4n4s1p" : "v2n2s1");
+        if (int rc = oneshot_launch(h, vid, nslots, iters, &oneshot, err)) return rc;
         // Anti-absorption, first choice: the narrowest wider variant whose live set exceeds
-        // 2x L2 (output identical; measured honest and as fast).  Not with a user grid.
-        if (h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 && absorbs(h, vid, nslots, iters)) {
+        // 2x L2 (output identical; measured honest and as fast).  Not with a user grid, and
+        // not needed on a one-shot grid, whose resident set already clears it.
+        if (!oneshot && h->epoch_iters == 0 && h->grid_warps == 0 && h->cta_warps == 0 &&
+            absorbs(h, vid, nslots, iters)) {
             int widest = vid;
             bool found = false;
             for (const char *nm : kWideNames) {
@@ -242,6 +290,8 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
                 if ((h->count + wp - 1) / wp >= max_grid_warps(h, widest)) vid = widest;
             }
         }
+    } else if (int rc = oneshot_launch(h, vid, nslots, iters, &oneshot, err)) {
+        return rc;
     }
     const Variant &v = kVariants[vid];
     BatchFn fn = h->output == 1 ? v.star : v.fn;
@@ -282,7 +332,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // and at most one unit per warp: nch = floor(warps / pieces), used only from 3 chunks
     // (measured on the Fig. 4 cells, profiles/r2_fig4.md).
     uint64_t nch = 0;
-    if (iters <= nslots) {
+    if (iters <= nslots && !oneshot) {
         if (h->chunk_iters > 0 && iters > (uint64_t)h->chunk_iters) {
             nch = (iters + h->chunk_iters - 1) / h->chunk_iters;  // PRNG_OPT_CHUNK_ITERS: forced
         } else if (h->time_parallel && iters >= 2 * kTpMinChunk) {
@@ -301,7 +351,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     // Anti-absorption, fallback: epoch-major order (batch_kernel_epoch) with E = R, so an
     // address is rewritten only one whole epoch (the full ring) later.
     uint64_t E = 0;
-    if (nch <= 1 && h->epoch_iters >= 0) {
+    if (nch <= 1 && h->epoch_iters >= 0 && !oneshot) {
         if (h->epoch_iters > 0)
             E = (uint64_t)h->epoch_iters;  // PRNG_OPT_EPOCH_ITERS: forced
         else if (absorbs(h, vid, nslots, iters, wps))
@@ -339,17 +389,28 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
         a.state_out = h->d_state2;  // chunks read d_state; the last chunk writes the other half
         units = a.npieces * C;
     }
-    const uint64_t rounds0 = (units + max_warps - 1) / max_warps;
-    uint64_t warps = (units + rounds0 - 1) / rounds0;
-    // Spread the warps over all SMs: with <= 8 warps per SM use one CTA per SM of
-    // ceil(warps / SMs) warps, else 256-thread CTAs.
-    uint64_t wpb = kBlock / 32;
-    if (warps <= (uint64_t)h->num_sms * wpb) wpb = std::max<uint64_t>(1, (warps + h->num_sms - 1) / h->num_sms);
-    if (h->cta_warps > 0) wpb = (uint64_t)h->cta_warps;  // PRNG_OPT_CTA_WARPS
-    uint64_t blocks = (warps + wpb - 1) / wpb;
+    uint64_t wpb, blocks;
+    if (oneshot) {  // one unit per warp, 4-warp CTAs over as many waves as it takes
+        wpb = kOneShotBlock / 32;
+        blocks = (units + wpb - 1) / wpb;
+    } else {
+        const uint64_t rounds0 = (units + max_warps - 1) / max_warps;
+        const uint64_t warps = (units + rounds0 - 1) / rounds0;
+        // Spread the warps over all SMs: with <= 8 warps per SM use one CTA per SM of
+        // ceil(warps / SMs) warps, else 256-thread CTAs.
+        wpb = kBlock / 32;
+        if (warps <= (uint64_t)h->num_sms * wpb) wpb = std::max<uint64_t>(1, (warps + h->num_sms - 1) / h->num_sms);
+        if (h->cta_warps > 0) wpb = (uint64_t)h->cta_warps;  // PRNG_OPT_CTA_WARPS
+        blocks = (warps + wpb - 1) / wpb;
+    }
+    if (blocks > 0x7FFFFFFFull) return set_err(err, PRNG_EINVAL, "grid of %llu CTAs", (unsigned long long)blocks);
     a.rounds = (uint32_t)((units + blocks * wpb - 1) / (blocks * wpb));
     h->last_kernel = vid;
     h->last_epoch = (uint32_t)E;
+    h->last_blocks = blocks;
+    h->last_threads = (uint32_t)(32 * wpb);
+    h->last_rounds = a.rounds;
+    h->last_one_shot = oneshot;
     if (int rc = prof_begin(h, s, PRNG_EV_RNG_KERNEL, err)) return rc;
     fn<<<(unsigned)blocks, (unsigned)(32 * wpb), 0, s>>>(a);
     if (a.jump) std::swap(h->d_state, h->d_state2);  // time-parallel: the final state is in the other half
@@ -423,6 +484,15 @@ int prng_last_launch(const prng_t *h, int *variant, uint32_t *epoch_iters, prng_
     if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
     if (variant) *variant = h->last_kernel;
     if (epoch_iters) *epoch_iters = h->last_epoch;
+    return ok(err);
+}
+int prng_last_grid(const prng_t *h, uint64_t *blocks, uint32_t *threads, uint32_t *rounds, int *one_shot,
+                   prng_err_t *err) {
+    if (!h) return set_err(err, PRNG_EINVAL, "NULL handle");
+    if (blocks) *blocks = h->last_blocks;
+    if (threads) *threads = h->last_threads;
+    if (rounds) *rounds = h->last_rounds;
+    if (one_shot) *one_shot = h->last_one_shot ? 1 : 0;
     return ok(err);
 }
 const char *prng_kernel_variant_name(int id) { return (id >= 0 && id < kNumVariants) ? kVariants[id].name : nullptr; }
@@ -617,6 +687,10 @@ int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err) {
             if (value < 0 || value > 1) return set_err(err, PRNG_EINVAL, "bad fused-seed flag");
             h->fused_seed = (int)value;
             break;
+        case PRNG_OPT_ONE_SHOT:
+            if (value < 0 || value > 2) return set_err(err, PRNG_EINVAL, "bad one-shot mode");
+            h->one_shot = (int)value;
+            break;
 
 
         default:
@@ -644,6 +718,7 @@ int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err
         case PRNG_OPT_PIECE_ORDER: *value = h->piece_order; break;
         case PRNG_OPT_EPOCH_ITERS: *value = h->epoch_iters; break;
         case PRNG_OPT_FUSED_SEED: *value = h->fused_seed; break;
+        case PRNG_OPT_ONE_SHOT: *value = h->one_shot; break;
 
 
         default: return set_err(err, PRNG_EINVAL, "unknown option %d", option);

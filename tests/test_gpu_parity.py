@@ -532,6 +532,10 @@ def test_auto_kernel_at_bench_shape(n, name):
         assert (P.prng_kernel_variant_name(ran), epoch) == (name, 0)
         if n == 1 << 24:
             assert slots == 512
+            # 65536 pieces: > 8 waves of resident one-shot warps -> one piece per warp
+            assert P.prng_last_grid(h) == (16384, 128, 1, True)
+        else:
+            assert not P.prng_last_grid(h)[3]
         last = P.prng_read_slot(h, (first + 999) % slots, n)
         g = np.random.default_rng(5).integers(0, n, 2000)
         want = np.array([oracle.sample(int(x), 999, SEED_PARITY) for x in g], dtype=np.uint64)
@@ -977,20 +981,25 @@ def _gpu_folds(row, gid0, chunk=1 << 27):
     return x & M64, s & M64, w & M64
 
 
-def _device_only_full_shape(numrn_total, gid_begin, count, numiter, seed, expect_kernel=None):
+def _device_only_full_shape(numrn_total, gid_begin, count, numiter, seed, expect_kernel=None, one_shot=1,
+                            expect_one_shot=None):
     """One device-only launch exactly as bench.py runs it (default kernel, default 64 GiB
-    rotating ring): for every iteration still in the ring, the XOR, the wrapping sum and the
-    gid-weighted sum of all its outputs (order-sensitive: a misplaced piece changes it), and
-    the whole last iteration and the final state element by element -- all against the
-    oracle's flat loop over the same gid range."""
+    rotating ring; PRNG_OPT_ONE_SHOT as given): for every iteration still in the ring, the
+    XOR, the wrapping sum and the gid-weighted sum of all its outputs (order-sensitive: a
+    misplaced piece changes it), and the whole last iteration and the final state element by
+    element -- all against the oracle's flat loop over the same gid range."""
     import torch
     h = P.prng_create_range(numrn_total, seed, gid_begin, count, 0)
     try:
+        P.prng_set_option(h, P.PRNG_OPT_ONE_SHOT, one_shot)
         P.prng_init(h)
         P.prng_generate(h, numiter)
         ran, epoch = P.prng_last_launch(h)
         if expect_kernel is not None:
             assert (P.prng_kernel_variant_name(ran), epoch) == expect_kernel
+        if expect_one_shot is not None:
+            blocks, threads, rounds, os_ = P.prng_last_grid(h)
+            assert os_ == expect_one_shot and (rounds == 1 if os_ else blocks <= 148 * 8), (blocks, threads, rounds)
         base, pitch, slots, first, end = P.prng_device_ring(h)
         assert end == numiter
         ring = torch.as_tensor(_DevArray(base, (slots, pitch)), device="cuda")
@@ -1012,24 +1021,29 @@ def _device_only_full_shape(numrn_total, gid_begin, count, numiter, seed, expect
 
 
 @pytest.mark.slow
-def test_config2_bench_shape_order_sensitive():
+@pytest.mark.parametrize("one_shot", [1, 0])
+def test_config2_bench_shape_order_sensitive(one_shot):
     """BASELINE config 2 = the bench step (numrn = 2^24, numiter = 1000, seed 0, the default
-    kernel "auto" -> v4n8s1a, 512-slot ring): every ring slot's three folds, the whole last
+    kernel "auto" -> v4n8s1a, 512-slot ring; by default on a one-shot grid, and on the
+    persistent grid with PRNG_OPT_ONE_SHOT 0): every ring slot's three folds, the whole last
     iteration and the state element by element, vs the oracle."""
-    _device_only_full_shape(1 << 24, 0, 1 << 24, 1000, 0, ("v4n8s1a", 0))
+    _device_only_full_shape(1 << 24, 0, 1 << 24, 1000, 0, ("v4n8s1a", 0), one_shot, bool(one_shot))
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("lg,name", [(25, "v4n8s1a"), (26, "v4n16s1"), (27, "v2n32s1")])
-def test_config4_rank_shapes_order_sensitive(lg, name):
+@pytest.mark.parametrize("lg,name,one_shot", [(25, "v4n8s1a", 1), (26, "v4n8s1a", 1), (27, "v4n8s1a", 1),
+                                              (25, "v4n8s1a", 0), (26, "v4n16s1", 0), (27, "v2n32s1", 0)])
+def test_config4_rank_shapes_order_sensitive(lg, name, one_shot):
     """BASELINE config 4 at its per-rank shapes: 2^28 over P = 8 / 4 / 2 ranks gives 2^25 /
-    2^26 / 2^27 gids per rank, 1000 iterations, default 64 GiB ring of 256 / 128 / 64 slots
-    (the anti-absorption rule picks v4n8s1a / v4n16s1 / v2n32s1).  The LAST rank's gid range
-    (up to gid 2^28 - 1), so the global-gid weights and the gid offset are exercised."""
+    2^26 / 2^27 gids per rank, 1000 iterations, default 64 GiB ring of 256 / 128 / 64 slots.
+    By default v4n8s1a on a one-shot grid, whose resident set clears 2 x L2 at every ring;
+    on the persistent grid (PRNG_OPT_ONE_SHOT 0) the anti-absorption rule picks v4n8s1a /
+    v4n16s1 / v2n32s1.  The LAST rank's gid range (up to gid 2^28 - 1), so the global-gid
+    weights and the gid offset are exercised."""
     n = 1 << lg
     P_ = (1 << 28) // n
     b, c = shard_range(1 << 28, P_ - 1, P_)
-    _device_only_full_shape(1 << 28, b, c, 1000, SEED_PARITY, (name, 0))
+    _device_only_full_shape(1 << 28, b, c, 1000, SEED_PARITY, (name, 0), one_shot, bool(one_shot))
 
 
 def _e2e_digest_run(numrn_total, gid_begin, count, numiter, seed, mode):
@@ -1476,3 +1490,117 @@ def test_fused_seed_top_of_gid_range_and_a3(fused):
     out2, st2 = _run_path("e2e", "auto", fused, 0, n, 4, 5, gid_begin=gb2, count=999)
     want2 = oracle.stream(n, 4, 5, gb2, 999)
     assert np.array_equal(out2, want2) and np.array_equal(st2, want2[-1])
+
+
+# ---------------------------------------------------------------- one-shot grids (PRNG_OPT_ONE_SHOT)
+@pytest.mark.parametrize("out_kind", [0, 1])
+@pytest.mark.parametrize("kname", ALL_NAMES)
+def test_one_shot_every_variant(kname, out_kind):
+    """PRNG_OPT_ONE_SHOT 2 forces the one-shot grid (one piece per warp, 4-warp CTAs, many
+    waves) at a small ragged size: every slot of a ring that holds the whole launch and the
+    state vs the oracle, for every variant and both output transforms; the grid reported by
+    prng_last_grid is the one-shot one."""
+    n, i = 300007, 13
+    h = P.prng_create(n, SEED_PARITY)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_KERNEL, _kid(kname))
+        P.prng_set_option(h, P.PRNG_OPT_OUTPUT, out_kind)
+        P.prng_set_option(h, P.PRNG_OPT_ONE_SHOT, 2)
+        P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, i)
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        blocks, threads, rounds, os_ = P.prng_last_grid(h)
+        vid, _ = P.prng_last_launch(h)
+        npt = {"v4n8s1a": 8, "v4n4s1p": 4, "v4n8s1": 8, "v4n16s1": 16, "v2n32s1": 32, "v2n4s1": 4, "v4n4s1": 4,
+               "v2n2s1": 2}[P.prng_kernel_variant_name(vid)]
+        pieces = -(-n // (32 * npt))
+        assert (os_, threads, rounds, blocks) == (True, 128, 1, -(-pieces // 4))
+        _, _, slots, first, _ = P.prng_device_ring(h)
+        got = np.stack([P.prng_read_slot(h, (first + k) % slots, n) for k in range(i)])
+        st = P.prng_read_state(h, n)
+    finally:
+        P.prng_destroy(h)
+    assert np.array_equal(got, (oracle.stream_star if out_kind else oracle.stream)(n, i, SEED_PARITY))
+    assert np.array_equal(st, oracle.stream(n, i, SEED_PARITY)[-1])
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("path", ["e2e", "host", "device_stream", "zerocopy"])
+def test_one_shot_launch_forms(path, fused):
+    """One-shot grids under the other launch forms (the e2e double buffer, the host array, a
+    caller device buffer on another stream, zero-copy), with fused and separate a1, on a
+    gid-offset ragged handle."""
+    import torch
+    n, gb, i = 100001, 33, 7
+    cnt = n - gb - 4   # 99964: 32-B rows for zero-copy, a ragged last piece
+    h = P.prng_create_range(n, 11, gb, cnt)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_ONE_SHOT, 2)
+        P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, fused)
+        P.prng_init(h)
+        if path in ("e2e", "zerocopy"):
+            P.prng_set_option(h, P.PRNG_OPT_MODE, P.PRNG_MODE_ZEROCOPY if path == "zerocopy" else P.PRNG_MODE_OVERLAP2)
+            P.prng_set_option(h, P.PRNG_OPT_BATCH_ITERS, 3)
+            out = np.zeros((i, cnt), np.uint64)
+            P.prng_generate(h, i, P.SINK_COPY, P.CopySink(out.ctypes.data_as(P.P64), cnt, 0, i, gb))
+        elif path == "host":
+            out = np.zeros((i, cnt), np.uint64)
+            P.prng_generate_host(h, i, out, cnt, i)
+        else:
+            pitch = (cnt + 3) // 4 * 4
+            buf = torch.zeros((i, pitch), dtype=torch.int64, device="cuda")
+            P.prng_generate_device(h, i, buf.data_ptr(), pitch, i, torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            out = buf[:, :cnt].cpu().numpy().view(np.uint64).copy()
+        assert P.prng_last_grid(h)[3]
+        st = P.prng_read_state(h, cnt)
+    finally:
+        P.prng_destroy(h)
+    want = oracle.stream(n, i, 11, gb, cnt)
+    assert np.array_equal(out, want) and np.array_equal(st, want[-1])
+
+
+def test_one_shot_not_where_it_would_absorb_or_chunk():
+    """The one-shot grid is not used where the rule keeps other forms: a launch that wraps a
+    small ring (its resident set would rewrite L2-resident lines: the anti-absorption rule
+    decides), a time-parallel launch (auto, few pieces), a user-fixed grid, forced epochs or
+    chunks, or PRNG_OPT_ONE_SHOT 0."""
+    cases = [  # (n, iters, ring slots, extra options, expect one-shot)
+        (1 << 20, 80, 8, [(P.PRNG_OPT_ONE_SHOT, 2)], False),           # wraps 8 slots: would absorb
+        (4000, 1000, 0, [], False),                                      # auto: time-parallel chunks
+        (300007, 9, 9, [(P.PRNG_OPT_GRID_WARPS, 296)], False),          # user grid
+        (300007, 9, 9, [(P.PRNG_OPT_EPOCH_ITERS, 3)], False),           # forced epochs
+        (300007, 9, 9, [(P.PRNG_OPT_CHUNK_ITERS, 4)], False),           # forced chunks
+        (300007, 9, 9, [], False),                                       # auto: < 8 waves of pieces
+        (300007, 9, 9, [(P.PRNG_OPT_ONE_SHOT, 2)], True),
+        (300007, 9, 9, [(P.PRNG_OPT_ONE_SHOT, 0)], False),
+    ]
+    for n, i, R, opts, expect in cases:
+        h = P.prng_create(n, 4)
+        try:
+            P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, R)
+            for o, v in opts:
+                P.prng_set_option(h, o, v)
+            P.prng_init(h)
+            P.prng_generate(h, i)
+            assert P.prng_last_grid(h)[3] == expect, (n, i, R, opts)
+            _, _, slots, first, _ = P.prng_device_ring(h)
+            assert np.array_equal(P.prng_read_slot(h, (first + i - 1) % slots, n), oracle.stream(n, i, 4)[-1])
+        finally:
+            P.prng_destroy(h)
+
+
+def test_one_shot_option_roundtrip_and_errors():
+    h = P.prng_create(100, 0)
+    try:
+        assert P.prng_get_option(h, P.PRNG_OPT_ONE_SHOT) == 1
+        for v in (0, 2, 1):
+            P.prng_set_option(h, P.PRNG_OPT_ONE_SHOT, v)
+            assert P.prng_get_option(h, P.PRNG_OPT_ONE_SHOT) == v
+        for bad in (-1, 3):
+            with pytest.raises(P.PrngError) as e:
+                P.prng_set_option(h, P.PRNG_OPT_ONE_SHOT, bad)
+            assert e.value.code == P.PRNG_EINVAL
+        assert P.prng_last_grid(h) == (0, 0, 0, False)
+    finally:
+        P.prng_destroy(h)
