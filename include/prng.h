@@ -249,9 +249,11 @@ enum prng_mode {
 int prng_set_option(prng_t *h, int option, int64_t value, prng_err_t *err);
 int prng_get_option(const prng_t *h, int option, int64_t *value, prng_err_t *err);
 
-/* Measure a short list of (kernel variant, warps per SM) candidates on this handle's
- * device-only ring (probe_iters iterations each, 0 = auto: ~16 GiB of output) and keep
- * the fastest as PRNG_OPT_KERNEL + PRNG_OPT_GRID_WARPS.  The probes consume the device
+/* Measure a short list of (kernel variant, grid) candidates -- persistent grids of 4 or 8
+ * warps per SM and one-shot grids -- on this handle's device-only ring (probe_iters
+ * iterations each, 0 = auto: ~16 GiB of output) and keep the fastest as PRNG_OPT_KERNEL +
+ * PRNG_OPT_GRID_WARPS (a persistent winner) or PRNG_OPT_KERNEL + PRNG_OPT_ONE_SHOT 2 with
+ * PRNG_OPT_GRID_WARPS 0 (a one-shot winner).  The probes consume the device
  * state, so the handle must be prng_init'ed again afterwards (generate returns
  * PRNG_ESTATE otherwise).  best_gbs (may be NULL) gets the winner's probe GB/s. */
 int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err);

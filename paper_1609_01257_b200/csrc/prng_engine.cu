@@ -877,9 +877,10 @@ static int generate_device_only(prng *h, uint64_t numiter, prng_err_t *err) {
 // state array is consumed, so the handle needs prng_init afterwards.
 static const struct {
     const char *variant;
-    int warps_per_sm;
+    int warps_per_sm;  // persistent grid of this many warps per SM; 0: one-shot grid
 } kTuneCandidates[] = {{"v4n8s1a", 4}, {"v4n4s1p", 4}, {"v4n4s1", 4},  {"v2n4s1", 4}, {"v2n4s1", 8},
-                       {"v4n8s1", 4},  {"v4n16s1", 4}, {"v2n32s1", 8}, {"v2n2s1", 4}};
+                       {"v4n8s1", 4},  {"v4n16s1", 4}, {"v2n32s1", 8}, {"v2n2s1", 4}, {"v4n8s1a", 0},
+                       {"v4n16s1", 0}};
 
 extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, prng_err_t *err) {
     if (int rc = check_handle(h, err, false)) return rc;
@@ -897,12 +898,15 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
     double best = -1;
     int best_k = h->kernel;
     int64_t best_w = h->grid_warps;
+    const int saved_one_shot = h->one_shot;
+    int best_os = h->one_shot;
     int rc = PRNG_OK;
     for (const auto &c : kTuneCandidates) {
         const int k = variant_id(c.variant);
         if (k < 0) continue;
         h->kernel = k;
-        h->grid_warps = (int64_t)c.warps_per_sm * h->num_sms;
+        h->grid_warps = (int64_t)c.warps_per_sm * h->num_sms;  // 0: no user grid ...
+        h->one_shot = c.warps_per_sm ? saved_one_shot : 2;     // ... and a one-shot grid
         double cand = 0;
         for (int rep = 0; rep < 3 && !rc; ++rep) {
             cudaEventRecord(e0, h->s_gen);
@@ -925,6 +929,7 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
             best = cand;
             best_k = k;
             best_w = h->grid_warps;
+            best_os = h->one_shot;
         }
     }
     cudaEventDestroy(e0);
@@ -932,6 +937,7 @@ extern "C" int prng_autotune(prng_t *h, uint64_t probe_iters, double *best_gbs, 
     h->profile = saved_profile;
     h->kernel = best_k;
     h->grid_warps = best_w;
+    h->one_shot = rc ? saved_one_shot : best_os;
     h->inited = false;  // the probes consumed the state: prng_init before generating
     h->pos = 0;
     if (rc) return rc;

@@ -33,15 +33,19 @@ cases = [  # (n, iters, variant, mode, output, device-ring slots, PRNG_OPT_EPOCH
 # cases also run with the separate seed kernel (PRNG_OPT_FUSED_SEED 0), and every other case
 # reads the state between prng_init and the device-only generate (the pending seeds are
 # then materialised by seed_kernel and the launch does not seed)
-cases = [c + (1,) for c in cases] + [
-    (70001, 40, "auto", P.PRNG_MODE_OVERLAP2, 1, 16, 7, 0),   # separate a1: epochs, star
-    (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 1000, 0, 0),  # separate a1: time-parallel
-    (4100, 7, "v4n4s1p", P.PRNG_MODE_SERIAL, 0, 16, 0, 0),    # separate a1: ping-pong
+cases = [c + (1, 1) for c in cases] + [
+    (70001, 40, "auto", P.PRNG_MODE_OVERLAP2, 1, 16, 7, 0, 1),   # separate a1: epochs, star
+    (1000, 600, "v2n4s1", P.PRNG_MODE_OVERLAP2, 0, 1000, 0, 0, 1),  # separate a1: time-parallel
+    (4100, 7, "v4n4s1p", P.PRNG_MODE_SERIAL, 0, 16, 0, 0, 1),    # separate a1: ping-pong
+    # one-shot grids (PRNG_OPT_ONE_SHOT 2): one piece per warp, 4-warp CTAs, many waves
+    (300007, 9, "v4n8s1a", P.PRNG_MODE_OVERLAP2, 0, 16, 0, 1, 2),  # ragged last CTA / piece
+    (200001, 7, "v2n32s1", P.PRNG_MODE_OVERLAP1, 1, 16, 0, 0, 2),  # wide pieces, star, separate a1
 ]
 bad = 0
-for ci, (n, it, v, mode, out, slots, epoch, fused) in enumerate(cases):
+for ci, (n, it, v, mode, out, slots, epoch, fused, one_shot) in enumerate(cases):
     h = P.prng_create(n, 3)
     P.prng_set_option(h, P.PRNG_OPT_FUSED_SEED, fused)
+    P.prng_set_option(h, P.PRNG_OPT_ONE_SHOT, one_shot)
     P.prng_set_option(h, P.PRNG_OPT_KERNEL, names.index(v))
     P.prng_set_option(h, P.PRNG_OPT_OUTPUT, out)
     P.prng_set_option(h, P.PRNG_OPT_MODE, mode)
@@ -59,7 +63,8 @@ for ci, (n, it, v, mode, out, slots, epoch, fused) in enumerate(cases):
     P.prng_generate(h, it)  # device only through the ring
     ok = ok and np.array_equal(P.prng_read_state(h, n), oracle.stream(n, it, 3)[-1])
     vid, e = P.prng_last_launch(h)
+    grid_one_shot = P.prng_last_grid(h)[3]
     P.prng_destroy(h)
-    print(n, it, v, mode, out, slots, epoch, "fused", fused, "ran", names[vid], "E", e, "ok" if ok else "MISMATCH", flush=True)
+    print(n, it, v, mode, out, slots, epoch, "fused", fused, "one_shot", grid_one_shot, "ran", names[vid], "E", e, "ok" if ok else "MISMATCH", flush=True)
     bad += not ok
 sys.exit(1 if bad else 0)
