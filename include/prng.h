@@ -219,13 +219,14 @@ enum prng_option {
                                   `init` kernel; its interval is INIT_KERNEL in the
                                   profile, as in Fig. 5).                                   */
     PRNG_OPT_ONE_SHOT = 18     /* grid of natural-order launches with many more pieces than
-                                  one wave of resident warps: 1 (default) auto -- from 5
-                                  waves of the one-shot grid's resident warps on (2^23
-                                  work-items for v4n8s1a), one piece per warp on a
-                                  multi-wave grid of 4-warp CTAs that the hardware
-                                  dispatches in order (measured 2-8 % more write bandwidth
-                                  than the persistent grid from 2^23 work-items, 5 % more
-                                  under the power cap); 0: always the
+                                  one wave of resident warps: 1 (default) auto -- from 4
+                                  waves of the one-shot grid's resident warps on (3 CTAs
+                                  per SM; 2^20 work-items with v4n4s1p, 2^21 with v4n8s1a),
+                                  one piece per warp on a multi-wave grid of 4-warp CTAs
+                                  that the hardware dispatches in order (measured 2-7 %
+                                  more write bandwidth than the persistent grid from 2^20
+                                  work-items, 5.6 % more under the power cap; DESIGN.md
+                                  §5); 0: always the
                                   persistent one-wave grid; 2: one-shot whenever the launch
                                   form allows it (natural order, no PRNG_OPT_GRID_WARPS /
                                   CTA_WARPS / EPOCH_ITERS / CHUNK_ITERS, no L2-absorbing

@@ -122,6 +122,7 @@ struct prng {
     // grids, PRNG_OPT_ONE_SHOT); 0 = not queried yet
     int oneshot_blocks_per_sm[2][prng_detail::kMaxVariants] = {};  // [output transform][variant]
     int one_shot = 1;               // PRNG_OPT_ONE_SHOT: 0 off, 1 auto, 2 always (when allowed)
+    size_t oneshot_smem = 0;        // dynamic shared memory per one-shot CTA (residency cap)
     uint64_t last_blocks = 0;       // grid of the last batch launch (prng_last_grid)
     uint32_t last_threads = 0, last_rounds = 0;
     bool last_one_shot = false;

@@ -199,22 +199,30 @@ constexpr uint64_t kAutoNarrowBelow = 1ull << 15;
 constexpr uint64_t kTpMinChunk = 48;
 
 // One-shot grids (PRNG_OPT_ONE_SHOT, profiles/r2_write_ceiling.md §7): a
-// natural-order launch with many more pieces than one wave of the persistent grid holds
-// runs one piece per warp on a multi-wave grid of 4-warp CTAs, which the hardware
-// dispatches in order as earlier CTAs retire.  Measured on B200 (raw_r2/m32-m35): at 2^23
-// to 2^27 work-items 2-8 % more DRAM write bandwidth than the persistent 4-warps-per-SM
-// grid in a burst, and 5 % more sustained under the power cap (6.79 vs 6.44 TB/s at the
-// bench shape); at 2^21-2^22 (<= 3 waves of v4n8s1a's 5328 resident one-shot warps) 1-5 %
-// slower.  Used from this many waves of resident one-shot warps on (2^23 = 6.2 waves).
-constexpr uint64_t kOneShotMinWaves = 5;
+// natural-order launch with many more pieces than one wave holds runs one piece per warp
+// on a multi-wave grid of 4-warp CTAs, which the hardware dispatches in order as earlier
+// CTAs retire.  Measured on B200 with 3 resident CTAs per SM (raw_r2/m38): from 2^20 to
+// 2^24 work-items 2-7 % more DRAM write bandwidth than the persistent 4-warps-per-SM grid
+// in a burst (2^21 x 1000: a tie) and 5.6 % more sustained under the power cap at the
+// bench shape (7.09-7.10 vs 6.72 TB/s); at 2^19 (2.3 waves) 3-11 % slower.  Used from this
+// many waves of resident one-shot warps on (2^20 with v4n4s1p / 2^21 with v4n8s1a: 4.6).
+constexpr uint64_t kOneShotMinWaves = 4;
 
 // Resident warps of a one-shot grid of variant vid (occupancy at kOneShotBlock threads of
 // the instantiation this launch will run), queried once per handle.
+// Resident one-shot CTAs per SM are capped at kOneShotCtasPerSm by giving each CTA an
+// (unused) share of the SM's shared memory: more, shorter waves.  Measured (raw_r2/m37):
+// at 2^22 work-items the uncapped grid (9 CTAs/SM, 3 waves) writes 6.41-6.43 TB/s, capped
+// at 2 / 3 / 4 / 6 CTAs/SM 6.97-7.18 (persistent: 6.97-7.0); at 2^23-2^24 every cap is
+// within 1 % of the uncapped grid (7.1-7.25 burst, 6.94-7.0 sustained).
+constexpr int kOneShotCtasPerSm = 3;
+
 static int oneshot_capacity(prng *h, int vid, BatchFn fn, uint64_t *warps, prng_err_t *err) {
     int &b = h->oneshot_blocks_per_sm[h->output == 1 ? 1 : 0][vid];
     if (b == 0) {
         int q = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, fn, kOneShotBlock, 0));
+        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->oneshot_smem));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, fn, kOneShotBlock, h->oneshot_smem));
         b = std::max(q, 1);
     }
     *warps = (uint64_t)b * h->num_sms * (kOneShotBlock / 32);
@@ -412,7 +420,7 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     h->last_rounds = a.rounds;
     h->last_one_shot = oneshot;
     if (int rc = prof_begin(h, s, PRNG_EV_RNG_KERNEL, err)) return rc;
-    fn<<<(unsigned)blocks, (unsigned)(32 * wpb), 0, s>>>(a);
+    fn<<<(unsigned)blocks, (unsigned)(32 * wpb), oneshot ? h->oneshot_smem : 0, s>>>(a);
     if (a.jump) std::swap(h->d_state, h->d_state2);  // time-parallel: the final state is in the other half
     CU(cudaGetLastError());
     h->seed_pending = false;  // every launch writes the whole state array
@@ -541,6 +549,14 @@ prng_t *prng_create_range(uint64_t numrn_total, uint64_t seed, uint64_t gid_begi
     if ((e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
         return bail("cudaDeviceGetAttribute(SMs)", e);
     cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, dev);
+    {   // dynamic shared memory per one-shot CTA that leaves room for kOneShotCtasPerSm
+        int sm_smem = 0, reserved = 0, cta_max = 0;
+        cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+        cudaDeviceGetAttribute(&cta_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int per = sm_smem / kOneShotCtasPerSm - reserved;
+        h->oneshot_smem = (size_t)std::max(0, std::min(per, cta_max));
+    }
     for (int i = 0; i < kNumVariants; ++i) {
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm[i], kVariants[i].fn, kBlock, 0)) !=
             cudaSuccess)

@@ -456,15 +456,18 @@ def test_epoch_order(kname, epoch, out_kind):
             assert np.array_equal(st, state)
 
 
-# (numrn, iterations, ring slots, epoch option, expected (variant, epoch length)); L2 = 126 MB
-# on B200, 592 warps: live set = R x min(592, pieces) x bytes per warp-iteration vs 2 x L2.
+# (numrn, iterations, ring slots, epoch option, expected (variant, epoch length)[, one-shot
+# option]); L2 = 126 MB on B200; persistent grid 592 warps, one-shot grid 1776 resident warps:
+# live set = R x min(resident warps, pieces) x bytes per warp-iteration vs 2 x L2.
 ANTI_ABSORPTION = [
     (300007, 1000, 16, 0, ("v4n4s1p", 16)),  # no wide variant clears 2 x L2 and the widest has < 1 piece
                                              # per warp: epoch order on the default, E = R
     (300007, 1000, 16, -1, ("v4n4s1p", 0)),  # -1: natural order (absorbing) on request
     (300007, 40, 64, 0, ("v4n4s1p", 0)),     # no wrap inside the launch: nothing to absorb
     (1 << 20, 80, 64, 0, ("v2n32s1", 0)),    # 64 x 592 x 8 KiB = 310 MB: the 8 KiB variant
-    (1 << 20, 310, 300, 0, ("v4n8s1", 0)),   # 300 x 592 x 2 KiB = 364 MB: the 2 KiB variant
+    (1 << 20, 310, 300, 0, ("v4n4s1p", 0)),  # one-shot grid (8192 pieces >= 4 waves): its resident set
+                                             # 300 x 1776 x 1 KiB = 545 MB clears 2 x L2 unchanged
+    (1 << 20, 310, 300, 0, ("v4n8s1", 0), 0),  # persistent grid: 300 x 592 x 2 KiB = 364 MB, the 2 KiB variant
     ((1 << 20) + 77, 80, 64, 0, ("v2n32s1", 0)),  # ragged
     (1 << 20, 50, 8, 0, ("v2n32s1", 8)),     # none clears 2 x L2: epoch order on the widest, E = R
     (1 << 21, 100, 40, 0, ("v2n32s1", 0)),   # widest at 8 warps/SM: 40 x 1184 x 8 KiB = 388 MB
@@ -476,19 +479,22 @@ def _slot_digest(row):
     return int(np.bitwise_xor.reduce(row)), int(row.sum(dtype=np.uint64))
 
 
-@pytest.mark.parametrize("n,i,R,epoch_opt,expect", ANTI_ABSORPTION)
+@pytest.mark.parametrize("case", ANTI_ABSORPTION)
 @pytest.mark.parametrize("out_kind", [0, 1])
-def test_anti_absorption_rule(n, i, R, epoch_opt, expect, out_kind):
+def test_anti_absorption_rule(case, out_kind):
     """The device-only launch wraps a ring of R slots: the default variant is replaced by a
     wider one (or epoch order) so that no address is rewritten while its line can still be
     in L2.  The kernel that ran (prng_last_launch), the R slots still in the
     ring (element by element for small runs, else per-slot XOR / sum digests against the
     oracle's per-iteration digests plus sampled elements) and the final state."""
+    n, i, R, epoch_opt, expect = case[:5]
+    one_shot = case[5] if len(case) > 5 else 1
     small = n * i <= 1 << 26
     if out_kind and not small:
         pytest.skip("scrambled output checked on the small cases")
     h = P.prng_create(n, SEED_PARITY)
     try:
+        P.prng_set_option(h, P.PRNG_OPT_ONE_SHOT, one_shot)
         P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, R)
         P.prng_set_option(h, P.PRNG_OPT_EPOCH_ITERS, epoch_opt)
         P.prng_set_option(h, P.PRNG_OPT_OUTPUT, out_kind)
@@ -533,10 +539,12 @@ def test_auto_kernel_at_bench_shape(n, name):
         assert (P.prng_kernel_variant_name(ran), epoch) == (name, 0)
         if n == 1 << 24:
             assert slots == 512
-            # 65536 pieces: > 8 waves of resident one-shot warps -> one piece per warp
+            # 65536 pieces, 37 waves of one-shot warps (3 CTAs of 4 warps per SM) -> one piece per warp
             assert P.prng_last_grid(h) == (16384, 128, 1, True)
-        else:
-            assert not P.prng_last_grid(h)[3]
+        import torch
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        pieces = -(-n // (32 * {"v4n8s1a": 8, "v4n4s1p": 4, "v2n2s1": 2}[name]))
+        assert P.prng_last_grid(h)[3] == (pieces >= 4 * 3 * 4 * sms), (n, pieces)  # kOneShotMinWaves
         last = P.prng_read_slot(h, (first + 999) % slots, n)
         g = np.random.default_rng(5).integers(0, n, 2000)
         want = np.array([oracle.sample(int(x), 999, SEED_PARITY) for x in g], dtype=np.uint64)

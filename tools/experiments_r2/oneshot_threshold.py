@@ -53,7 +53,7 @@ def run(n, it, mode, reps):
 
 res = {}
 for rnd in range(3):
-    for lg in (21, 22, 23, 24):
+    for lg in (19, 20, 21, 22, 23, 24):
         for it in (100, 1000):
             for mode in (0, 2):
                 b, m, grid, v, ep, mhz = run(1 << lg, it, mode, 5)
