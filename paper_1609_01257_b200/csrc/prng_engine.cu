@@ -264,7 +264,17 @@ int launch_batch(prng *h, uint64_t *dst, uint64_t pitch, uint64_t nslots, uint64
     bool oneshot = false;
     if (vid == 0) {  // "auto"
         vid = variant_id(h->count >= kAutoWideFrom ? "v4n8s1a" : h->count >= kAutoNarrowBelow ? "v4n4s1p" : "v2n2s1");
+        // One-shot grid on the default variant, else on the narrowest wider one whose
+        // one-shot resident set clears 2x L2 when the launch wraps a small ring (2^27 per
+        // GPU through 64 slots: v4n16s1; 2^28 through 32: v2n32s1)
         if (int rc = oneshot_launch(h, vid, nslots, iters, &oneshot, err)) return rc;
+        for (const char *nm : kWideNames) {
+            if (oneshot) break;
+            const int w = variant_id(nm);
+            if (kVariants[w].npt * kVariants[w].vec <= kVariants[vid].npt * kVariants[vid].vec) continue;
+            if (int rc = oneshot_launch(h, w, nslots, iters, &oneshot, err)) return rc;
+            if (oneshot) vid = w;
+        }
         // Anti-absorption, first choice: the narrowest wider variant whose live set exceeds
         // 2x L2 (output identical; measured honest and as fast).  Not with a user grid, and
         // not needed on a one-shot grid, whose resident set already clears it.

@@ -1040,14 +1040,15 @@ def test_config2_bench_shape_order_sensitive(one_shot):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("lg,name,one_shot", [(25, "v4n8s1a", 1), (26, "v4n8s1a", 1), (27, "v4n8s1a", 1),
+@pytest.mark.parametrize("lg,name,one_shot", [(25, "v4n8s1a", 1), (26, "v4n8s1a", 1), (27, "v4n16s1", 1),
                                               (25, "v4n8s1a", 0), (26, "v4n16s1", 0), (27, "v2n32s1", 0)])
 def test_config4_rank_shapes_order_sensitive(lg, name, one_shot):
     """BASELINE config 4 at its per-rank shapes: 2^28 over P = 8 / 4 / 2 ranks gives 2^25 /
     2^26 / 2^27 gids per rank, 1000 iterations, default 64 GiB ring of 256 / 128 / 64 slots.
-    By default v4n8s1a on a one-shot grid, whose resident set clears 2 x L2 at every ring;
-    on the persistent grid (PRNG_OPT_ONE_SHOT 0) the anti-absorption rule picks v4n8s1a /
-    v4n16s1 / v2n32s1.  The LAST rank's gid range (up to gid 2^28 - 1), so the global-gid
+    By default a one-shot grid (1776 resident warps), on v4n8s1a while its live set clears
+    2 x L2 and on v4n16s1 at 64 slots (64 x 1776 x 2 KiB = 233 MB would not); on the
+    persistent grid (PRNG_OPT_ONE_SHOT 0, 592 warps) the anti-absorption rule picks
+    v4n8s1a / v4n16s1 / v2n32s1.  The LAST rank's gid range (up to gid 2^28 - 1), so the global-gid
     weights and the gid offset are exercised."""
     n = 1 << lg
     P_ = (1 << 28) // n
