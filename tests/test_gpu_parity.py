@@ -1614,3 +1614,30 @@ def test_one_shot_option_roundtrip_and_errors():
         assert P.prng_last_grid(h) == (0, 0, 0, False)
     finally:
         P.prng_destroy(h)
+
+
+def test_one_shot_widens_instead_of_absorbing():
+    """A wrapping launch whose default variant's one-shot resident set would rewrite
+    L2-resident lines takes the narrowest wider variant that clears 2 x L2, still on the
+    one-shot grid (2^20 through 40 slots, forced one-shot: v4n4s1p's 40 x 1776 x 1 KiB =
+    73 MB would absorb, v4n16s1's 40 x 1776 x 4 KiB = 291 MB does not); every slot still
+    held and the state vs the oracle."""
+    n, i, R = 1 << 20, 100, 40
+    h = P.prng_create(n, 8)
+    try:
+        P.prng_set_option(h, P.PRNG_OPT_ONE_SHOT, 2)
+        P.prng_set_option(h, P.PRNG_OPT_RING_SLOTS, R)
+        P.prng_init(h)
+        P.prng_generate(h, i)
+        vid, ep = P.prng_last_launch(h)
+        assert (P.prng_kernel_variant_name(vid), ep) == ("v4n16s1", 0)
+        assert P.prng_last_grid(h)[3]
+        _, _, slots, first, _ = P.prng_device_ring(h)
+        rows = {k: P.prng_read_slot(h, (first + k) % slots, n) for k in range(i - R, i)}
+        st = P.prng_read_state(h, n)
+    finally:
+        P.prng_destroy(h)
+    want = oracle.stream(n, i, 8)
+    for k, row in rows.items():
+        assert np.array_equal(row, want[k]), k
+    assert np.array_equal(st, want[-1])
