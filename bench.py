@@ -310,7 +310,7 @@ def ncu_traffic(variant, epoch):
     p = os.path.join(ROOT, "profiles", "ncu_batch_kernel.json")
     m = re.fullmatch(r"v(\d+)n(\d+)s1([ap]?)", variant or "")
     if not os.path.exists(p) or not m or epoch:
-        return None, None
+        return None, None, None
     with open(p) as f:
         d = json.load(f)
     # batch_kernel<VEC, NPT, OUT, AL, PP>; ncu spells bools as true/false or 1/0
@@ -324,8 +324,8 @@ def ncu_traffic(variant, epoch):
         return args == want
 
     if not any(same_kernel(k.get("kernel", "")) for k in d.get("kernels", [])):
-        return None, None
-    return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+        return None, None, None
+    return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch"), d.get("thread_instructions_per_number")
 
 
 # ---------------------------------------------------------------- oracle timing (CPU)
@@ -478,13 +478,14 @@ def run_ours(a, D):
     achieved = algo_bytes / (kmean * 1e-3) / 1e9
     ran, epoch = P.prng_last_launch(h)  # the kernel the timed launches ran ("auto", anti-absorption)
     vname = P.prng_kernel_variant_name(ran)
-    traffic, traffic_algo = ncu_traffic(vname, epoch)
+    traffic, traffic_algo, inst_per_number = ncu_traffic(vname, epoch)
     if traffic_algo is not None and int(traffic_algo) != algo_bytes:
-        traffic = None  # the committed capture is of another shape
+        traffic = inst_per_number = None  # the committed capture is of another shape
     kname = ("prngk::batch_kernel_epoch<" + vname + f", E={epoch}>" if epoch else "prngk::batch_kernel<" + vname + ">")
     gb_, gt_, gr_, g1_ = P.prng_last_grid(h)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kname,
+                "thread_instructions_per_number": inst_per_number,
                 "grid_warps": grid_warps or "variant default", "autotune_probe_gbs": tune_gbs,
                 "grid": {"ctas": gb_, "threads_per_cta": gt_, "rounds_per_warp": gr_,
                          "form": "one-shot (one piece per warp, CTAs dispatched in order)" if g1_

@@ -54,6 +54,10 @@ def full(rep, out, algo):
     res = {"source": rep, "kernels": kern,
            "dram_bytes_per_launch": k0.get("dram__bytes_read.sum", 0) + k0.get("dram__bytes_write.sum", 0),
            "algorithmic_bytes_per_launch": algo}
+    if algo and isinstance(k0.get("smsp__inst_executed.sum"), float):
+        # thread-instructions per number = warp-instructions x 32 / (n x T),
+        # n x T = algorithmic bytes / 8
+        res["thread_instructions_per_number"] = k0["smsp__inst_executed.sum"] * 32 / (algo / 8)
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps({k: v for k, v in res.items() if k != "kernels"}))
 
