@@ -1,6 +1,6 @@
 #!/bin/bash
-# Closing check of a session: build, the whole GPU suite (fast + slow), smoke, compute-sanitizer
-# over tools/sanitize_cases.py, bench (+ reference arm) at the driver's 20 / 5 steps, ncu
+# Closing check of a session: build, the whole GPU suite (fast + slow), smoke, bench
+# (+ reference arm) at the driver's 20 / 5 steps, ncu
 # launch list + --set full capture of the bench kernel.
 # Usage (repo root, on the GPU box): bash tools/gpu_close.sh TAG
 set -x
@@ -10,9 +10,8 @@ python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 timeout 1500 python -m pytest tests -q -m "gpu and not slow" > $OUT/pytest_gpu_fast.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu_fast.log
 timeout 2400 python -m pytest tests -q -m "gpu and slow" --durations=0 > $OUT/pytest_gpu_slow.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu_slow.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
-for T in memcheck racecheck synccheck initcheck; do
-  timeout 900 compute-sanitizer --tool $T python tools/sanitize_cases.py > $OUT/san_$T.txt 2>&1; echo "rc=$?" >> $OUT/san_$T.txt
-done
+# compute-sanitizer is closed on this GPU pool (r2q: it refuses to run, rc 86); the
+# sanitizer cases stay in tools/sanitize_cases.py / tools/gpu_san.sh for pools that allow it.
 timeout 900 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
