@@ -56,6 +56,7 @@ DEF_NUMRN_MULTI = 1 << 28    # BASELINE configs 4 / 5 (total over N > 1 GPUs)
 DEF_NUMITER = 1000           # configs 2 / 3 / 4
 DEF_NUMITER_C5 = 100         # config 5 (e2e at N > 1)
 REF_SAMPLE_ITERS = 64        # reference arm / cpu_baseline: iterations per sampled step
+CPU_REPS = 6                 # cpu_baseline: reference-arm steps timed back to back (~10 s of 1-core work)
 REF_SAMPLE_GIDS = 1 << 24    # ... over at most this many gids of the workload
 
 
@@ -143,6 +144,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probes", action="store_true")
     ap.add_argument("--cpu-numiter", type=int, default=REF_SAMPLE_ITERS, help="oracle sample: iterations")
+    ap.add_argument("--cpu-reps", type=int, default=CPU_REPS,
+                    help="cpu_baseline: the oracle sample run this many times back to back (~10 s at 2^24 gids)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--output", type=int, default=0, help="0 = the state (paper); 1 = xorshift64* scrambled (NEXT-3)")
     ap.add_argument("--no-numa-bind", action="store_true", help="keep the process's CPU affinity")
@@ -329,29 +332,36 @@ def ncu_traffic(variant, epoch):
 
 
 # ---------------------------------------------------------------- oracle timing (CPU)
-def cpu_baseline(numrn, count, numiter, seed):
+def cpu_baseline(numrn, count, numiter, seed, reps=1):
+    """The oracle sample `reps` times back to back (each rep = one --impl reference step)."""
     import oracle
     t = time.perf_counter()
-    oracle.digest(numrn, numiter, seed, 0, count)
+    for _ in range(reps):
+        oracle.digest(numrn, numiter, seed, 0, count)
     dt = time.perf_counter() - t
-    return count * numiter / dt, dt
+    return reps * count * numiter / dt, dt
 
 
-def cpu_baseline_all_cores(numrn, count, numiter, seed):
+def cpu_baseline_all_cores(numrn, count, numiter, seed, reps=1):
     """The same oracle function, unchanged, on one contiguous gid shard per host core
     (threads: ctypes releases the GIL), as BASELINE.md's CPU plan asks."""
     import oracle
     cores = len(os.sched_getaffinity(0))
     oracle.lib()
     shards = [shard_range(count, r, cores) for r in range(cores)]
-    th = [threading.Thread(target=oracle.digest, args=(numrn, numiter, seed, b, c)) for b, c in shards if c]
+
+    def work(b, c):
+        for _ in range(reps):
+            oracle.digest(numrn, numiter, seed, b, c)
+
+    th = [threading.Thread(target=work, args=(b, c)) for b, c in shards if c]
     t = time.perf_counter()
     for x in th:
         x.start()
     for x in th:
         x.join()
     dt = time.perf_counter() - t
-    return count * numiter / dt, dt, len(th)
+    return reps * count * numiter / dt, dt, len(th)
 
 
 def ref_sample(numrn):
@@ -592,14 +602,15 @@ def run_ours(a, D):
     cpu = None
     if D.rank == 0 and D.world == 1 and not a.no_cpu:
         ccnt, cni = ref_sample(numrn)
-        v, dt = cpu_baseline(numrn, ccnt, a.cpu_numiter, a.seed)
+        reps = max(1, a.cpu_reps)
+        v, dt = cpu_baseline(numrn, ccnt, a.cpu_numiter, a.seed, reps)
         cpu = {"value": v, "unit": "numbers/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
-               "sample": f"gids [0, {ccnt}) of numrn={numrn} x numiter={a.cpu_numiter} ({dt:.1f} s, digest-folded, "
-                         f"1 thread): the same sample as --impl reference"}
-        va, dta, nth = cpu_baseline_all_cores(numrn, ccnt, 4 * a.cpu_numiter, a.seed)
+               "sample": f"{reps} x (gids [0, {ccnt}) of numrn={numrn} x numiter={a.cpu_numiter}) ({dt:.1f} s, "
+                         f"digest-folded, 1 thread): {reps} steps of the --impl reference sample"}
+        va, dta, nth = cpu_baseline_all_cores(numrn, ccnt, a.cpu_numiter, a.seed, 4 * reps)
         cpu["all_cores"] = {"value": va, "unit": "numbers/s", "cores": nth, "cpu_model": cpu["cpu_model"],
-                            "sample": f"gids [0, {ccnt}) x numiter={4 * a.cpu_numiter} ({dta:.1f} s), one gid shard "
-                                      f"per thread"}
+                            "sample": f"{4 * reps} x (gids [0, {ccnt}) x numiter={a.cpu_numiter}) ({dta:.1f} s), one "
+                                      f"gid shard per thread"}
 
     if D.rank == 0:
         line = {
