@@ -9,7 +9,10 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libprng_b200.so")
+# PRNG_B200_CHECKED=1: the test-only checked build (device bounds checks that trap,
+# -DPRNG_CHECKED, prng_kernels.cuh) in libprng_b200_checked.so; the package then loads it.
+CHECKED = os.environ.get("PRNG_B200_CHECKED") == "1"
+LIB = os.path.join(PKG, "libprng_b200_checked.so" if CHECKED else "libprng_b200.so")
 SOURCES = [os.path.join(CSRC, f) for f in
            ("prng_engine.cu", "prng_pipeline.cu", "prng_prof.cpp", "prng_sinks.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "prng_kernels.cuh"), os.path.join(CSRC, "engine_internal.h"),
@@ -74,20 +77,24 @@ def build_probes(force: bool = False) -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     build_probes(force)
     if not force and not needs_build():
-        build_cli()
+        if not CHECKED:
+            build_cli()
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
+    cmd = [NVCC, *NVCC_FLAGS, *(["-DPRNG_CHECKED"] if CHECKED else []), "-I", os.path.join(ROOT, "include"), "-o",
+           tmp, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed ({r.returncode}): {' '.join(cmd)}")
-    with open(os.path.join(CSRC, "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+    if not CHECKED:
+        with open(os.path.join(CSRC, "ptxas_info.txt"), "w") as f:
+            f.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
     os.replace(tmp, LIB)
-    build_cli(force=True)
+    if not CHECKED:  # the CLI links the default library
+        build_cli(force=True)
     return LIB
 
 

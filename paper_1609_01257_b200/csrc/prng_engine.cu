@@ -1009,6 +1009,28 @@ int prng_read_state(prng_t *h, uint64_t *host_dst, prng_err_t *err) {
     return ok(err);
 }
 
+#ifdef PRNG_CHECKED
+// Checked build only (tools/gpu_checked.sh, tests/test_gpu_parity.py): the negative control
+// of the kernels' bounds checks.  One natural-order launch into a one-slot ring whose pitch
+// (= its allocation) is 4 u64 short of the handle's count, so the last vector of the piece
+// holding the last gids falls outside it: the check must trap, and the call returns
+// PRNG_ECUDA (the context is then unusable: run it in a process of its own).
+int prng_checked_selftest(prng_t *h, prng_err_t *err) {
+    if (int rc = check_handle(h, err, false)) return rc;
+    if (h->count < 8 || h->count % 4) return set_err(err, PRNG_EINVAL, "selftest needs count %% 4 == 0, >= 8");
+    const uint64_t pitch = h->count - 4;
+    uint64_t *buf = nullptr;
+    CU(cudaMalloc(&buf, pitch * sizeof(uint64_t)));
+    h->kernel = variant_id("v4n4s1");
+    int rc = launch_batch(h, buf, pitch, 1, 0, 2, true, h->s_gen, err);
+    const cudaError_t e = cudaStreamSynchronize(h->s_gen);
+    cudaFree(buf);
+    if (rc) return rc;
+    if (e != cudaSuccess) return set_err(err, PRNG_ECUDA, "selftest launch: %s", cudaGetErrorString(e));
+    return ok(err);  // not reached when the checks work
+}
+#endif
+
 // ---------------------------------------------------------------------------- a6 capture
 int prng_prof_events(const prng_t *hc, uint64_t cap, uint32_t *name_id, double *start_s, double *end_s,
                      uint64_t *n_out, double *wall_s, prng_err_t *err) {

@@ -25,8 +25,34 @@
 // No code here is shared with oracle/ (the CPU definition); see DESIGN.md §2.
 #pragma once
 #include <cstdint>
+#ifdef PRNG_CHECKED
+#include <cstdio>
+#endif
 
 namespace prngk {
+
+// ---------------------------------------------------------------- checked build
+// -DPRNG_CHECKED (libprng_b200_checked.so, PRNG_B200_CHECKED=1; tests only): every global
+// store and state load of the seed / batch kernels is checked against its launch's
+// arguments -- inside the ring of nslots x pitch, column + width <= count, aligned to its
+// vector width; state index + width <= count -- and traps on a violation.  compute-sanitizer
+// is closed on the GPU pool, so the kernels carry their own bounds checks.
+// The default build compiles them out.
+#ifdef PRNG_CHECKED
+__device__ __noinline__ void check_fail(const char *what, const void *p, uint64_t v, uint64_t n) {
+    printf("prng bounds violation: %s at %p (index %llu, width %llu), block %u thread %u\n", what, p,
+           (unsigned long long)v, (unsigned long long)n, blockIdx.x, threadIdx.x);
+    __trap();
+}
+#define PRNG_CHK(cond, what, p, v, n) \
+    do {                               \
+        if (!(cond)) ::prngk::check_fail(what, p, v, n); \
+    } while (0)
+#else
+#define PRNG_CHK(cond, what, p, v, n) \
+    do {                               \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------- the method's arithmetic
 // A1: Wang's 32-bit multiplicative hash ("hash32shiftmult"), P:173 [wang1997inthash].
@@ -142,8 +168,10 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
         const uint64_t s0 = seed64(g, key_hi, key_lo);
         if (i + 1 < a.count) {
             const uint64_t s1 = seed64(g + 1u, key_hi, key_lo);
+            PRNG_CHK(((uintptr_t)(a.state + i) & 15) == 0, "seed store", a.state + i, i, 2);
             st_v2(a.state + i, s0, s1);
         } else {
+            PRNG_CHK(i < a.count, "seed store", a.state + i, i, 1);
             a.state[i] = s0;
         }
     }
@@ -182,6 +210,22 @@ struct BatchArgs {
     uint64_t gid_begin;
 };
 
+// Checked build: a store of n u64 at p into the launch's ring (or zero-copy host half).
+__device__ __forceinline__ void chk_ring(const BatchArgs &a, const uint64_t *p, int n) {
+#ifdef PRNG_CHECKED
+    const uint64_t off = (uint64_t)(p - a.dst);  // wraps to a huge value below dst
+    const bool ok = p >= a.dst && off + n <= (uint64_t)a.nslots * a.pitch && off % a.pitch + n <= a.count &&
+                    ((uintptr_t)p % (8u * n)) == 0;
+    PRNG_CHK(ok, "ring store", p, off, n);
+#endif
+}
+// ... and an access of n u64 at state index idx (state, state_out).
+__device__ __forceinline__ void chk_state(const BatchArgs &a, const uint64_t *base, uint64_t idx, int n) {
+#ifdef PRNG_CHECKED
+    PRNG_CHK(idx + n <= a.count && ((uintptr_t)(base + idx) % (8u * n)) == 0, "state access", base + idx, idx, n);
+#endif
+}
+
 // The start states of a lane's NPT gids (handle-relative base, VEC-wide groups vs apart):
 // seeds computed in registers (a1 fused) or loaded from the state array.  Gids at or past
 // `count` (the ragged last piece, PARTIAL only) get 0 and are never stored.
@@ -203,6 +247,7 @@ __device__ __forceinline__ void start_states(const BatchArgs &a, uint64_t base, 
     } else if constexpr (FULLP) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
+            chk_state(a, a.state, base + (uint64_t)v * vs, VEC);
             if constexpr (NC)
                 load_vec<VEC>(a.state + base + (uint64_t)v * vs, x + v * VEC);
             else
@@ -333,6 +378,7 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
             if constexpr (MODE == FULL) {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
+                    chk_ring(a, p + v * vs, VEC);
                     if constexpr (OUT == 0) {
                         store_vec<VEC>(p + v * vs, src + v * VEC);
                     } else {
@@ -347,7 +393,10 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
                 for (int v = 0; v < NV; ++v)
 #pragma unroll
                     for (int e = 0; e < VEC; ++e)
-                        if (base + (uint64_t)v * vs + e < a.count) p[v * vs + e] = emit<OUT>(src[v * VEC + e]);
+                        if (base + (uint64_t)v * vs + e < a.count) {
+                            chk_ring(a, p + v * vs + e, 1);
+                            p[v * vs + e] = emit<OUT>(src[v * VEC + e]);
+                        }
             }
         }
         cta_barrier<AL>(bar_threads);
@@ -390,7 +439,10 @@ __device__ __forceinline__ void run_piece(const BatchArgs &a, const Unit &u, uin
     if (u.state_out) {
         if constexpr (MODE == FULL) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) store_vec<VEC>(u.state_out + base + (uint64_t)v * vs, x + v * VEC);
+            for (int v = 0; v < NV; ++v) {
+                chk_state(a, u.state_out, base + (uint64_t)v * vs, VEC);
+                store_vec<VEC>(u.state_out + base + (uint64_t)v * vs, x + v * VEC);
+            }
         } else {
 #pragma unroll
             for (int v = 0; v < NV; ++v)
@@ -499,6 +551,7 @@ __device__ __forceinline__ void epoch_unit(const BatchArgs &a, uint64_t *x, uint
                 uint64_t y[VEC];
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) y[q] = emit<OUT>(x[v * VEC + q]);
+                chk_ring(a, p + v * 32 * VEC, VEC);
                 store_vec<VEC>(p + v * 32 * VEC, y);
             }
         } else {
@@ -506,7 +559,10 @@ __device__ __forceinline__ void epoch_unit(const BatchArgs &a, uint64_t *x, uint
             for (int v = 0; v < NV; ++v)
 #pragma unroll
                 for (int q = 0; q < VEC; ++q)
-                    if (base + (uint64_t)v * 32 * VEC + q < a.count) p[v * 32 * VEC + q] = emit<OUT>(x[v * VEC + q]);
+                    if (base + (uint64_t)v * 32 * VEC + q < a.count) {
+                        chk_ring(a, p + v * 32 * VEC + q, 1);
+                        p[v * 32 * VEC + q] = emit<OUT>(x[v * VEC + q]);
+                    }
         }
         cta_barrier<AL>(bar_threads);
         if (++slot == a.nslots) {  // warp-uniform
@@ -570,7 +626,10 @@ __global__ void __launch_bounds__(256) batch_kernel_epoch(BatchArgs a) {
                 else
                     epoch_unit<VEC, NPT, OUT, true, false>(a, x, base, slot_begin, t_count, emit_first, bar_threads);
 #pragma unroll
-                for (int v = 0; v < NV; ++v) store_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+                for (int v = 0; v < NV; ++v) {
+                    chk_state(a, a.state, base + (uint64_t)v * 32 * VEC, VEC);
+                    store_vec<VEC>(a.state + base + (uint64_t)v * 32 * VEC, x + v * VEC);
+                }
             } else {  // the ragged last piece
                 start_states<VEC, NPT, false>(a, base, 32ull * VEC, x, seed_now);
                 epoch_unit<VEC, NPT, OUT, false>(a, x, base, slot_begin, t_count, emit_first, bar_threads);

@@ -227,3 +227,39 @@ def test_sink_digest_folds():
     assert _sink_call("prng_sink_digest", d, 13, 1, 0, 6, data) != 0   # iteration 13 outside [10, 13)
     d2 = P.DigestSink(x.ctypes.data_as(P.P64), s.ctypes.data_as(P.P64), 10, 3, None)
     assert _sink_call("prng_sink_digest", d2, 10, 1, 0, 6, data) == 0   # no weighted output
+
+
+def _sass_functions(path):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+    funcs, name = {}, None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            name = m.group(1)
+            funcs[name] = []
+        elif name:
+            funcs[name].append(line)
+    return funcs
+
+
+def test_checked_build_traps_behind_every_kernel_store():
+    """tools/gpu_checked.sh's library (the kernels' own bounds checks; compute-sanitizer is
+    closed on the GPU pool): -DPRNG_CHECKED builds libprng_b200_checked.so, in which every
+    seed / batch / epoch kernel carries a trap behind its ring-store and state-access checks;
+    the default library has none."""
+    import sys
+    env = dict(os.environ, PRNG_B200_CHECKED="1")
+    r = subprocess.run([sys.executable, "-c", "from paper_1609_01257_b200 import _build; print(_build.build())"],
+                       env=env, capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    path = r.stdout.strip().splitlines()[-1]
+    assert path.endswith("libprng_b200_checked.so") and path != P.LIB
+    checked = _sass_functions(path)
+    plain = _sass_functions(P.LIB)
+    assert set(checked) == set(plain)
+    hot = [f for f in checked if re.search(r"seed_kernel|batch_kernel", f)]
+    assert len(hot) >= 20, hot
+    for f in hot:
+        assert any("TRAP" in ln for ln in checked[f]), f"no trap in checked {f}"
+    for f in plain:
+        assert not any("TRAP" in ln for ln in plain[f]), f"trap in the default build's {f}"
