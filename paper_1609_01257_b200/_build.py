@@ -12,7 +12,9 @@ CSRC = os.path.join(PKG, "csrc")
 # PRNG_B200_CHECKED=1: the test-only checked build (device bounds checks that trap,
 # -DPRNG_CHECKED, prng_kernels.cuh) in libprng_b200_checked.so; the package then loads it.
 CHECKED = os.environ.get("PRNG_B200_CHECKED") == "1"
-LIB = os.path.join(PKG, "libprng_b200_checked.so" if CHECKED else "libprng_b200.so")
+DEFAULT_LIB = os.path.join(PKG, "libprng_b200.so")
+CHECKED_LIB = os.path.join(PKG, "libprng_b200_checked.so")
+LIB = CHECKED_LIB if CHECKED else DEFAULT_LIB
 SOURCES = [os.path.join(CSRC, f) for f in
            ("prng_engine.cu", "prng_pipeline.cu", "prng_prof.cpp", "prng_sinks.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "prng_kernels.cuh"), os.path.join(CSRC, "engine_internal.h"),
@@ -31,10 +33,10 @@ NVCC_FLAGS = [
 ]
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
@@ -74,28 +76,31 @@ def build_probes(force: bool = False) -> str:
     return PROBES_LIB
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    build_probes(force)
-    if not force and not needs_build():
-        if not CHECKED:
+def build(force: bool = False, verbose: bool = False, checked: bool = CHECKED, probes: bool = True) -> str:
+    """The hot-path library (checked: its bounds-checked test build) and the probes."""
+    if probes:
+        build_probes(force)
+    lib = CHECKED_LIB if checked else DEFAULT_LIB
+    if not force and not needs_build(lib):
+        if not checked:
             build_cli()
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, *(["-DPRNG_CHECKED"] if CHECKED else []), "-I", os.path.join(ROOT, "include"), "-o",
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, *(["-DPRNG_CHECKED"] if checked else []), "-I", os.path.join(ROOT, "include"), "-o",
            tmp, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed ({r.returncode}): {' '.join(cmd)}")
-    if not CHECKED:
+    if not checked:
         with open(os.path.join(CSRC, "ptxas_info.txt"), "w") as f:
             f.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    if not CHECKED:  # the CLI links the default library
+    os.replace(tmp, lib)
+    if not checked:  # the CLI links the default library
         build_cli(force=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
