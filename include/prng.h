@@ -343,6 +343,17 @@ int prng_prof_export(uint64_t nevents, const uint32_t *name_id, const double *st
  * host link) are measurement tools, not part of the hot path: they live in their own
  * library, libprng_probes.so (include/prng_probes.h). */
 
+#ifdef PRNG_CHECKED
+/* Test-only, and exported only by the bounds-checked build libprng_b200_checked.so
+ * (-DPRNG_CHECKED; PRNG_B200_CHECKED=1 makes the Python package load it).  In that build every
+ * ring store and state access of the seed / batch / epoch kernels is checked against its
+ * launch's arguments and traps on a violation.  This is the negative control: one launch into
+ * a one-slot ring 4 u64 short of the handle's count (count % 4 == 0, >= 8) must trap, so the
+ * call returns PRNG_ECUDA.  The CUDA context is then unusable: call it in a process of its
+ * own (tests/test_checked_build.py). */
+int prng_checked_selftest(prng_t *h, prng_err_t *err);
+#endif
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,11 +15,15 @@ from oracle import prof as oprof
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared_functions(headers=("prng.h", "prng_sinks.h")):
+def _declared_functions(headers=("prng.h", "prng_sinks.h"), checked=False):
+    """Functions include/ declares; declarations under #ifdef PRNG_CHECKED (the test-only
+    checked build's) only with checked=True."""
     names = set()
     for h in headers:
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        if not checked:
+            src = re.sub(r"#ifdef PRNG_CHECKED.*?#endif", "", src, flags=re.S)
         for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(prng_\w+)\s*\(", src, flags=re.M):
             names.add(m.group(1))
     return names
@@ -254,6 +258,9 @@ def test_checked_build_traps_behind_every_kernel_store():
     assert r.returncode == 0, r.stderr[-2000:]
     path = r.stdout.strip().splitlines()[-1]
     assert path.endswith("libprng_b200_checked.so") and path != P.LIB
+    exported = _exported(path)
+    assert _declared_functions(checked=True) <= exported
+    assert "prng_checked_selftest" in exported and "prng_checked_selftest" not in _exported(P.LIB)
     checked = _sass_functions(path)
     plain = _sass_functions(P.LIB)
     assert set(checked) == set(plain)
